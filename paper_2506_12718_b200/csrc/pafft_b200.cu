@@ -1,0 +1,1124 @@
+// libpafft_b200: host runtime behind include/pafft_b200.h.
+//
+// Owns plans (device twiddle tables + pass schedule, replacing Plan::Plan,
+// core.cpp:93-127), prepared filters (prepare_filter, convolution.cpp:9-14),
+// and issues the pass kernels (pass.cuh) for convolve_permfree
+// (convolution.cpp:45-52), convolve_standard (:37-43) and the transforms
+// (transform.cpp:8-26).  No CPU compute fallback exists: every transform runs
+// in the sm_100a kernels; the host only builds tables and moves buffers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pafft_b200.h"
+#include "pass.cuh"
+#include "registry.h"
+
+using namespace pafft_b200;
+
+namespace {
+
+// ------------------------------------------------------------ errors --
+thread_local std::string g_err;
+thread_local size_t g_err_dim = 0, g_err_extent = 0;
+thread_local uint64_t g_perm_passes = 0;
+thread_local uint64_t g_launches = 0;
+
+pafft_status fail(pafft_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (expr);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(PAFFT_CUDA_ERROR, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),   \
+                        __FILE__, __LINE__);                                                        \
+    } while (0)
+
+#define ST_TRY(expr)                      \
+    do {                                  \
+        pafft_status s_ = (expr);         \
+        if (s_ != PAFFT_OK) return s_;    \
+    } while (0)
+
+// ---------------------------------------------------------- registry --
+Registry& registry() {
+    static Registry reg;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        register_r2_f64(reg);
+        register_r3_f64(reg);
+        register_r4_f64(reg);
+        register_r5_f64(reg);
+        register_r8_f64(reg);
+        register_r2_f32(reg);
+        register_r3_f32(reg);
+        register_r4_f32(reg);
+        register_r5_f32(reg);
+        register_r8_f32(reg);
+    });
+    return reg;
+}
+
+const KernelEntry* find_kernel(int prec, int radix, int R, int kind) {
+    for (const auto& e : registry())
+        if (e.prec == prec && e.radix == radix && e.R == R && e.kind == kind) return &e;
+    return nullptr;
+}
+
+int max_stages_compiled(int radix) {
+    int best = 0;
+    for (const auto& e : registry()) {
+        if (e.radix != radix || e.prec != 0) continue;
+        int s = 0;
+        for (int v = e.R; v > 1; v /= radix) ++s;
+        best = std::max(best, s);
+    }
+    return best;
+}
+
+bool radix_ok(unsigned r) { return r == 2 || r == 3 || r == 4 || r == 5 || r == 8; }
+
+// ------------------------------------------------------------- tables --
+// exp(-2 pi i e / K) in long double, rounded once (TwiddleTable semantics,
+// core.cpp:84-91, at higher internal precision).
+inline void root(unsigned long long e, unsigned long long K, long double& c, long double& s) {
+    const long double pi = 3.141592653589793238462643383279502884L;
+    const unsigned long long g = e % K;
+    const long double a = -2.0L * pi * (long double)g / (long double)K;
+    c = cosl(a);
+    s = sinl(a);
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+struct PassDesc {
+    int kind = 0;
+    int axis = 0, a = 0, s = 0;
+    int R = 0, R1 = 1, R2 = 1, R3 = 1;
+    long long K0 = 0, L = 0, sq = 1, C = 1;
+    int contig = 0, W = 1, NT = 32;
+    size_t smem = 0;
+    int ext = 0;
+    unsigned ext_bits = 0;
+    const void* ext_lo = nullptr;
+    const void* ext_hi = nullptr;
+    const void* tw1 = nullptr;
+    const void* tw2 = nullptr;
+    const void* fn = nullptr;
+};
+
+struct Group {
+    int axis, a, s;
+};
+
+}  // namespace
+
+struct pafft_plan_s {
+    unsigned radix = 0;
+    int rank = 0;
+    size_t dims[8] = {0};
+    unsigned depth[8] = {0};
+    size_t total = 0;
+    int prec = 0;
+    int device = 0;
+    size_t esize = 16;  // bytes per complex element
+    std::vector<Group> groups;                 // DIF order; last = contiguous axis-0 group
+    std::vector<std::unique_ptr<DevBuf>> owned;
+    std::map<long long, std::pair<const void*, const void*>> ext_tables;  // K0 -> (lo, hi)
+    std::map<int, std::pair<const void*, const void*>> int_tables;        // R -> (tw1, tw2)
+    std::map<long long, unsigned> ext_bits;
+    std::vector<uint32_t*> rev_dev;            // per-axis digit reversal maps (device)
+    // scratch for permutation / host pipelines
+    std::unique_ptr<DevBuf> scratch;
+    std::unique_ptr<DevBuf> stage[3];
+    cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+    std::mutex mu;
+    // pass schedules, built once at plan creation (immutable afterwards)
+    std::vector<PassDesc> pf, dif, dit_fwd, dit_conj;
+};
+
+struct pafft_filter_s {
+    pafft_plan_t plan = nullptr;  // key: (radix, dims, precision, device)
+    unsigned radix = 0;
+    int rank = 0;
+    size_t dims[8] = {0};
+    int prec = 0, device = 0;
+    std::unique_ptr<DevBuf> ghat;         // unscaled, plan precision
+    std::unique_ptr<DevBuf> ghat_scaled;  // x (1/N), plan precision
+};
+
+namespace {
+
+pafft_status alloc(pafft_plan_t p, size_t bytes, void** out) {
+    auto b = std::make_unique<DevBuf>();
+    CUDA_TRY(cudaMalloc(&b->p, bytes ? bytes : 16));
+    b->bytes = bytes;
+    *out = b->p;
+    p->owned.push_back(std::move(b));
+    return PAFFT_OK;
+}
+
+template <typename T>
+pafft_status upload_roots(pafft_plan_t p, const std::vector<long double>& re, const std::vector<long double>& im,
+                          const void** out) {
+    std::vector<cplx<T>> h(re.size());
+    for (size_t i = 0; i < re.size(); ++i) h[i] = cplx<T>{(T)re[i], (T)im[i]};
+    void* d;
+    ST_TRY(alloc(p, h.size() * sizeof(cplx<T>), &d));
+    CUDA_TRY(cudaMemcpy(d, h.data(), h.size() * sizeof(cplx<T>), cudaMemcpyHostToDevice));
+    *out = d;
+    return PAFFT_OK;
+}
+
+pafft_status upload(pafft_plan_t p, const std::vector<long double>& re, const std::vector<long double>& im,
+                    const void** out) {
+    return p->prec == 0 ? upload_roots<double>(p, re, im, out) : upload_roots<float>(p, re, im, out);
+}
+
+pafft_status ext_table(pafft_plan_t p, long long K0, PassDesc& d) {
+    auto it = p->ext_tables.find(K0);
+    if (it == p->ext_tables.end()) {
+        unsigned lg = 0;
+        while ((1ll << lg) < K0) ++lg;
+        const unsigned bits = (lg + 1) / 2;
+        const long long nlo = 1ll << bits;
+        const long long nhi = (K0 + nlo - 1) / nlo;
+        std::vector<long double> lr(nlo), li(nlo), hr(nhi), hi(nhi);
+        for (long long e = 0; e < nlo; ++e) root(e, K0, lr[e], li[e]);
+        for (long long h = 0; h < nhi; ++h) root((unsigned long long)h * nlo, K0, hr[h], hi[h]);
+        const void *lo, *hip;
+        ST_TRY(upload(p, lr, li, &lo));
+        ST_TRY(upload(p, hr, hi, &hip));
+        p->ext_tables[K0] = {lo, hip};
+        p->ext_bits[K0] = bits;
+        it = p->ext_tables.find(K0);
+    }
+    d.ext_lo = it->second.first;
+    d.ext_hi = it->second.second;
+    d.ext_bits = p->ext_bits[K0];
+    return PAFFT_OK;
+}
+
+pafft_status int_table(pafft_plan_t p, PassDesc& d) {
+    auto it = p->int_tables.find(d.R);
+    if (it == p->int_tables.end()) {
+        const int R = d.R, R1 = d.R1, R23 = d.R2 * d.R3, R3 = d.R3;
+        std::vector<long double> r1(R), i1(R), r2(R23), i2(R23);
+        for (int k1 = 0; k1 < R1; ++k1)
+            for (int m = 0; m < R23; ++m) root((unsigned long long)k1 * m, R, r1[k1 * R23 + m], i1[k1 * R23 + m]);
+        for (int k2 = 0; k2 < d.R2; ++k2)
+            for (int m3 = 0; m3 < R3; ++m3)
+                root((unsigned long long)k2 * m3, R23, r2[k2 * R3 + m3], i2[k2 * R3 + m3]);
+        const void *t1, *t2;
+        ST_TRY(upload(p, r1, i1, &t1));
+        ST_TRY(upload(p, r2, i2, &t2));
+        p->int_tables[R] = {t1, t2};
+        it = p->int_tables.find(R);
+    }
+    d.tw1 = it->second.first;
+    d.tw2 = it->second.second;
+    return PAFFT_OK;
+}
+
+long long ipow(long long b, int e) {
+    long long v = 1;
+    while (e-- > 0) v *= b;
+    return v;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+// Stage groups in DIF order (north_star item 4: per-axis passes, no global
+// transposes).  Strided axes first (any order is valid: modes commute,
+// SPEC.md:226), then axis 0 split so its last group is a contiguous block.
+void build_groups(pafft_plan_t p) {
+    const int maxs = max_stages_compiled((int)p->radix);
+    const int max_mid = std::min(maxs, env_int("PAFFT_MAX_MID_STAGES", maxs));
+    int max_str = maxs;
+    if (p->radix == 2) max_str = std::min(max_str, 11);
+    max_str = std::min(max_str, env_int("PAFFT_MAX_STRIDED_STAGES", max_str));
+    p->groups.clear();
+    for (int q = p->rank - 1; q >= 0; --q) {
+        const int t = (int)p->depth[q];
+        if (t == 0) continue;
+        const int lim = (q == 0) ? std::max(max_mid, 1) : std::max(max_str, 1);
+        if (q == 0 && t > max_mid) {
+            // outer strided groups, then the contiguous group (gets the remainder)
+            const int npass = (t + std::min(max_mid, max_str) - 1) / std::min(max_mid, max_str);
+            int rem = t, a = 0;
+            for (int i = 0; i < npass; ++i) {
+                const int s = (rem + (npass - i) - 1) / (npass - i);
+                p->groups.push_back({q, a, s});
+                a += s;
+                rem -= s;
+            }
+        } else {
+            const int npass = (t + lim - 1) / lim;
+            int rem = t, a = 0;
+            for (int i = 0; i < npass; ++i) {
+                const int s = (rem + (npass - i) - 1) / (npass - i);
+                p->groups.push_back({q, a, s});
+                a += s;
+                rem -= s;
+            }
+        }
+    }
+    // The CONV pass needs the last group to be contiguous (axis 0, L == 1).
+    // Axis-0 groups are emitted last, in ascending stage order; ensure the
+    // contiguous one ends the list even if axis 0 has extent 1.
+}
+
+pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
+    const long long n = (long long)p->dims[g.axis];
+    long long sq = 1;
+    for (int q = 0; q < g.axis; ++q) sq *= (long long)p->dims[q];
+    d.kind = kind;
+    d.axis = g.axis;
+    d.a = g.a;
+    d.s = g.s;
+    d.R = (int)ipow(p->radix, g.s);
+    d.K0 = n / ipow(p->radix, g.a);
+    d.L = d.K0 / d.R;
+    d.sq = sq;
+    d.C = d.L * sq;
+    d.contig = d.C == 1;
+    const KernelEntry* ke = find_kernel(p->prec, (int)p->radix, d.R, kind);
+    if (!ke) return fail(PAFFT_INVALID_ARGUMENT, "no kernel for radix %u R=%d kind %d", p->radix, d.R, kind);
+    d.fn = ke->fn;
+    d.R1 = ke->R1;
+    d.R2 = ke->R2;
+    d.R3 = ke->R3;
+    const int nstep = 1 + (d.R2 > 1) + (d.R3 > 1);
+    int gmax = d.R / d.R1;
+    if (d.R2 > 1) gmax = std::max(gmax, d.R / d.R2);
+    if (d.R3 > 1) gmax = std::max(gmax, d.R / d.R3);
+    const size_t budget = (size_t)env_int("PAFFT_SMEM_BUDGET", 110 * 1024);
+    const size_t col_bytes = (size_t)d.R * p->esize;
+    if (d.contig) {
+        int W = std::max(1, 256 / std::max(gmax, 1));
+        if (nstep > 1) W = (int)std::max<size_t>(1, std::min<size_t>(W, budget / col_bytes));
+        d.W = W;
+    } else {
+        int W = p->prec == 0 ? 8 : 16;
+        W = env_int("PAFFT_STRIDED_W", W);
+        if (nstep > 1) W = (int)std::max<size_t>(1, std::min<size_t>(W, budget / col_bytes));
+        d.W = (int)std::min<long long>(W, d.C);
+    }
+    const int work = gmax * d.W;
+    d.NT = std::min(256, std::max(32, (work + 31) / 32 * 32));
+    d.smem = nstep > 1 ? (size_t)d.R * d.W * p->esize : 0;
+    if (d.smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(d.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
+    d.ext = d.L > 1;
+    if (d.ext) ST_TRY(ext_table(p, d.K0, d));
+    if (nstep > 1) ST_TRY(int_table(p, d));
+    return PAFFT_OK;
+}
+
+template <typename T>
+pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
+                      const void* ghat, const void* mul, double scale, cudaStream_t st) {
+    PassArgs<T> a;
+    memset(&a, 0, sizeof a);
+    a.src = (const cplx<T>*)src;
+    a.dst = (cplx<T>*)dst;
+    const long long per_signal = (long long)p->total / ((long long)d.R * d.C);
+    a.panels = per_signal * (long long)batch;
+    a.panel_elems = (long long)d.R * d.C;
+    a.C = (int)d.C;
+    a.W = d.W;
+    a.contig = d.contig;
+    a.tiles_per_panel = d.contig ? 1 : (int)((d.C + d.W - 1) / d.W);
+    a.tiles = d.contig ? (a.panels + d.W - 1) / d.W : a.panels * a.tiles_per_panel;
+    a.ext = d.ext;
+    a.sq = (unsigned)d.sq;
+    a.ext_bits = d.ext_bits;
+    a.ext_lo = (const cplx<T>*)d.ext_lo;
+    a.ext_hi = (const cplx<T>*)d.ext_hi;
+    a.tw1 = (const cplx<T>*)d.tw1;
+    a.tw2 = (const cplx<T>*)d.tw2;
+    a.ghat = (const cplx<T>*)ghat;
+    a.N = (long long)p->total;
+    a.mul = (const cplx<T>*)mul;
+    a.scale = (T)scale;
+    a.has_scale = scale != 1.0;
+    if (a.tiles == 0) return PAFFT_OK;
+    const long long grid = std::min<long long>(a.tiles, 0x7fffffffll);
+    void* args[] = {&a};
+    CUDA_TRY(cudaLaunchKernel(d.fn, dim3((unsigned)grid), dim3(d.NT), args, d.smem, st));
+    ++g_launches;
+    return PAFFT_OK;
+}
+
+pafft_status launch(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
+                    const void* ghat, const void* mul, double scale, cudaStream_t st) {
+    return p->prec == 0 ? launch_t<double>(p, d, src, dst, batch, ghat, mul, scale, st)
+                        : launch_t<float>(p, d, src, dst, batch, ghat, mul, scale, st);
+}
+
+// ---------------------------------------------------- helper kernels --
+// Out-of-place digit-reversal gather: y[i] = x[(rev_1(i_1), ..., rev_d(i_d))]
+// (permute_tensor, permutation.cpp:46-90, as a pure gather; an involution).
+struct PermArgs {
+    int rank;
+    unsigned long long dims[8];
+    const uint32_t* rev[8];
+};
+
+template <typename V>
+__global__ void permute_kernel(const V* __restrict__ x, V* __restrict__ y, unsigned long long total,
+                               unsigned long long count, PermArgs pa) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < count;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long sig = i / total;
+        unsigned long long r = i - sig * total, src = 0, w = 1;
+        for (int q = 0; q < pa.rank; ++q) {
+            const unsigned long long n = pa.dims[q];
+            const unsigned long long iq = r % n;
+            r /= n;
+            src += (unsigned long long)__ldg(pa.rev[q] + iq) * w;
+            w *= n;
+        }
+        y[i] = x[sig * total + src];
+    }
+}
+
+template <typename T>
+__global__ void scale_convert_kernel(const double2* __restrict__ in, cplx<T>* __restrict__ out,
+                                     cplx<T>* __restrict__ out_scaled, double s, unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const double2 v = in[i];
+        if (out) out[i] = cplx<T>{(T)v.x, (T)v.y};
+        out_scaled[i] = cplx<T>{(T)(v.x * s), (T)(v.y * s)};
+    }
+}
+
+template <typename T>
+__global__ void scale_kernel(const cplx<T>* __restrict__ in, cplx<T>* __restrict__ out, double s,
+                             unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const cplx<T> v = in[i];
+        out[i] = cplx<T>{(T)(v.x * s), (T)(v.y * s)};
+    }
+}
+
+// y[i] = x[i] * g[i mod N]  (hadamard_inplace, convolution.cpp:23-35), used only
+// when the plan has no stages at all (every extent 1).
+template <typename T>
+__global__ void hadamard_kernel(const cplx<T>* __restrict__ x, const cplx<T>* __restrict__ g, cplx<T>* __restrict__ y,
+                                unsigned long long N, unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        y[i] = cmul(x[i], g[i % N]);
+}
+
+unsigned grid_for(unsigned long long n, int threads) {
+    const unsigned long long b = (n + threads - 1) / threads;
+    return (unsigned)std::min<unsigned long long>(std::max<unsigned long long>(b, 1), 148ull * 32);
+}
+
+pafft_status permute_dev(pafft_plan_t p, const void* x, void* y, size_t batch, cudaStream_t st) {
+    PermArgs pa;
+    memset(&pa, 0, sizeof pa);
+    pa.rank = p->rank;
+    for (int q = 0; q < p->rank; ++q) {
+        pa.dims[q] = p->dims[q];
+        pa.rev[q] = p->rev_dev[q];
+    }
+    const unsigned long long count = (unsigned long long)p->total * batch;
+    if (count == 0) return PAFFT_OK;
+    if (p->prec == 0)
+        permute_kernel<double2><<<grid_for(count, 256), 256, 0, st>>>((const double2*)x, (double2*)y, p->total,
+                                                                      count, pa);
+    else
+        permute_kernel<float2><<<grid_for(count, 256), 256, 0, st>>>((const float2*)x, (float2*)y, p->total,
+                                                                     count, pa);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    g_perm_passes += batch;
+    return PAFFT_OK;
+}
+
+pafft_status hadamard_dev(pafft_plan_t p, const void* x, const void* g, void* y, size_t batch, cudaStream_t st) {
+    const unsigned long long n = (unsigned long long)p->total * batch;
+    if (p->prec == 0)
+        hadamard_kernel<double><<<grid_for(n, 256), 256, 0, st>>>((const double2*)x, (const double2*)g, (double2*)y,
+                                                                  p->total, n);
+    else
+        hadamard_kernel<float><<<grid_for(n, 256), 256, 0, st>>>((const float2*)x, (const float2*)g, (float2*)y,
+                                                                 p->total, n);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    return PAFFT_OK;
+}
+
+pafft_status ensure(std::unique_ptr<DevBuf>& b, size_t bytes) {
+    if (b && b->bytes >= bytes) return PAFFT_OK;
+    b.reset();
+    auto nb = std::make_unique<DevBuf>();
+    CUDA_TRY(cudaMalloc(&nb->p, bytes ? bytes : 16));
+    nb->bytes = bytes;
+    b = std::move(nb);
+    return PAFFT_OK;
+}
+
+pafft_status set_device(pafft_plan_t p) {
+    CUDA_TRY(cudaSetDevice(p->device));
+    return PAFFT_OK;
+}
+
+bool key_match(pafft_filter_t f, pafft_plan_t p) {
+    if (f->radix != p->radix || f->rank != p->rank || f->prec != p->prec || f->device != p->device) return false;
+    for (int q = 0; q < p->rank; ++q)
+        if (f->dims[q] != p->dims[q]) return false;
+    return true;
+}
+
+// Pass sequences (built on demand from the stage groups).
+pafft_status passes_permfree(pafft_plan_t p, std::vector<PassDesc>& out) {
+    out.clear();
+    const size_t ng = p->groups.size();
+    if (ng == 0) return PAFFT_OK;
+    for (size_t i = 0; i + 1 < ng; ++i) {
+        PassDesc d;
+        ST_TRY(make_pass(p, p->groups[i], KIND_DIF, d));
+        out.push_back(d);
+    }
+    {
+        PassDesc d;
+        ST_TRY(make_pass(p, p->groups[ng - 1], KIND_CONV, d));
+        out.push_back(d);
+    }
+    for (size_t i = ng - 1; i-- > 0;) {
+        PassDesc d;
+        ST_TRY(make_pass(p, p->groups[i], KIND_DIT_CONJ, d));
+        out.push_back(d);
+    }
+    return PAFFT_OK;
+}
+
+// A (kind DIT_FWD) / A-bar (DIT_CONJ): reverse group order; A^T (DIF): group order.
+pafft_status passes_ladder(pafft_plan_t p, int kind, std::vector<PassDesc>& out) {
+    out.clear();
+    const size_t ng = p->groups.size();
+    for (size_t i = 0; i < ng; ++i) {
+        const Group& g = kind == KIND_DIF ? p->groups[i] : p->groups[ng - 1 - i];
+        PassDesc d;
+        ST_TRY(make_pass(p, g, kind, d));
+        out.push_back(d);
+    }
+    return PAFFT_OK;
+}
+
+// Runs a ladder (list of passes) src -> dst; the first pass reads src, the
+// rest run in place on dst.  Epilogue (mul / scale) on the last pass.
+pafft_status run_ladder(pafft_plan_t p, const std::vector<PassDesc>& ps, const void* src, void* dst, size_t batch,
+                        const void* mul, double scale, cudaStream_t st) {
+    if (ps.empty()) {
+        // n == 1 everywhere: identity transform (plus epilogue)
+        if (src != dst)
+            CUDA_TRY(cudaMemcpyAsync(dst, src, p->total * batch * p->esize, cudaMemcpyDeviceToDevice, st));
+        if (scale != 1.0 || mul) return fail(PAFFT_INVALID_ARGUMENT, "epilogue on an empty ladder");
+        return PAFFT_OK;
+    }
+    for (size_t i = 0; i < ps.size(); ++i) {
+        const bool last = i + 1 == ps.size();
+        ST_TRY(launch(p, ps[i], i == 0 ? src : dst, dst, batch, nullptr, last ? mul : nullptr, last ? scale : 1.0,
+                      st));
+    }
+    return PAFFT_OK;
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+extern "C" {
+
+const char* pafft_last_error(void) { return g_err.c_str(); }
+
+void pafft_last_error_dim(size_t* dim, size_t* extent) {
+    if (dim) *dim = g_err_dim;
+    if (extent) *extent = g_err_extent;
+}
+
+const char* pafft_build_info(void) {
+    return "pafft_b200 sm_100a (" __DATE__ " " __TIME__ ")";
+}
+
+uint64_t pafft_permutation_pass_count(void) { return g_perm_passes; }
+void pafft_reset_permutation_pass_count(void) { g_perm_passes = 0; }
+uint64_t pafft_kernel_launch_count(void) { return g_launches; }
+
+pafft_status pafft_digit_reverse(uint64_t j, unsigned radix, unsigned digits, uint64_t* out) {
+    uint64_t bound = 1;
+    for (unsigned s = 0; s < digits; ++s) bound *= radix;
+    if (j >= bound)
+        return fail(PAFFT_INDEX_OUT_OF_RANGE, "index %llu outside [0, %llu)", (unsigned long long)j,
+                    (unsigned long long)bound);
+    uint64_t o = 0;
+    for (unsigned s = 0; s < digits; ++s) {
+        o = o * radix + j % radix;
+        j /= radix;
+    }
+    *out = o;
+    return PAFFT_OK;
+}
+
+pafft_status pafft_plan_create(unsigned radix, const size_t* dims, int rank, int precision, int device,
+                               pafft_plan_t* out) {
+    if (!out) return fail(PAFFT_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    if (!radix_ok(radix))
+        return fail(PAFFT_INVALID_ARGUMENT, "radix must be 2, 3, 4, 5, or 8 (got %u)", radix);
+    if (rank <= 0) return fail(PAFFT_EMPTY_SHAPE, "shape has no dimensions");
+    if (rank > 8) return fail(PAFFT_INVALID_ARGUMENT, "rank %d exceeds 8", rank);
+    if (precision != PAFFT_F64 && precision != PAFFT_F32)
+        return fail(PAFFT_INVALID_ARGUMENT, "unknown precision %d", precision);
+    for (int q = 0; q < rank; ++q) {
+        size_t n = dims[q];
+        bool pow = n != 0;
+        while (pow && n % radix == 0) n /= radix;
+        pow = pow && n == 1;
+        if (!pow) {
+            g_err_dim = (size_t)q;
+            g_err_extent = dims[q];
+            return fail(PAFFT_NOT_A_POWER_OF_RADIX, "dimension %d has extent %zu, not a power of radix %u", q,
+                        dims[q], radix);
+        }
+        if (dims[q] > 0xffffffffull) return fail(PAFFT_INVALID_ARGUMENT, "dimension extent exceeds 32-bit range");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(PAFFT_NO_DEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+    }
+    if (device < 0) CUDA_TRY(cudaGetDevice(&device));
+    CUDA_TRY(cudaSetDevice(device));
+    auto p = std::make_unique<pafft_plan_s>();
+    p->radix = radix;
+    p->rank = rank;
+    p->prec = precision;
+    p->device = device;
+    p->esize = precision == PAFFT_F64 ? 16 : 8;
+    p->total = 1;
+    for (int q = 0; q < rank; ++q) {
+        p->dims[q] = dims[q];
+        p->total *= dims[q];
+        unsigned t = 0;
+        for (size_t n = dims[q]; n > 1; n /= radix) ++t;
+        p->depth[q] = t;
+    }
+    build_groups(p.get());
+    // all pass schedules now, so missing kernels surface at plan time
+    ST_TRY(passes_permfree(p.get(), p->pf));
+    ST_TRY(passes_ladder(p.get(), KIND_DIF, p->dif));
+    ST_TRY(passes_ladder(p.get(), KIND_DIT_FWD, p->dit_fwd));
+    ST_TRY(passes_ladder(p.get(), KIND_DIT_CONJ, p->dit_conj));
+    for (int q = 0; q < rank; ++q) {
+        std::vector<uint32_t> rev(dims[q]);
+        for (size_t j = 0; j < dims[q]; ++j) {
+            size_t v = j, o = 0;
+            for (unsigned s = 0; s < p->depth[q]; ++s) {
+                o = o * radix + v % radix;
+                v /= radix;
+            }
+            rev[j] = (uint32_t)o;
+        }
+        void* d;
+        ST_TRY(alloc(p.get(), rev.size() * 4, &d));
+        CUDA_TRY(cudaMemcpy(d, rev.data(), rev.size() * 4, cudaMemcpyHostToDevice));
+        p->rev_dev.push_back((uint32_t*)d);
+    }
+    for (auto& s : p->streams) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // table uploads above used pageable cudaMemcpy; make them visible to
+    // every stream (including non-blocking ones) before the plan is used
+    CUDA_TRY(cudaDeviceSynchronize());
+    *out = p.release();
+    return PAFFT_OK;
+}
+
+pafft_status pafft_plan_destroy(pafft_plan_t plan) {
+    if (!plan) return PAFFT_OK;
+    cudaSetDevice(plan->device);
+    for (auto& s : plan->streams)
+        if (s) cudaStreamDestroy(s);
+    delete plan;
+    return PAFFT_OK;
+}
+
+pafft_status pafft_plan_info(pafft_plan_t p, unsigned* radix, int* rank, size_t* dims, unsigned* depths,
+                             size_t* total, int* precision, int* device) {
+    if (!p) return fail(PAFFT_INVALID_ARGUMENT, "null plan");
+    if (radix) *radix = p->radix;
+    if (rank) *rank = p->rank;
+    for (int q = 0; q < p->rank; ++q) {
+        if (dims) dims[q] = p->dims[q];
+        if (depths) depths[q] = p->depth[q];
+    }
+    if (total) *total = p->total;
+    if (precision) *precision = p->prec;
+    if (device) *device = p->device;
+    return PAFFT_OK;
+}
+
+pafft_status pafft_plan_num_passes(pafft_plan_t p, int* n) {
+    *n = p->pf.empty() ? 1 : (int)p->pf.size();
+    return PAFFT_OK;
+}
+
+pafft_status pafft_plan_describe(pafft_plan_t p, char* buf, size_t len) {
+    const std::vector<PassDesc>& ps = p->pf;
+    std::string s;
+    const char* kn[] = {"DIF", "DIT_FWD", "DIT_CONJ", "CONV"};
+    for (const auto& d : ps) {
+        char line[256];
+        snprintf(line, sizeof line,
+                 "%s axis=%d stages=[%d,%d) R=%d(%dx%dx%d) K0=%lld L=%lld C=%lld %s W=%d NT=%d smem=%zu ext=%d\n",
+                 kn[d.kind], d.axis, d.a, d.a + d.s, d.R, d.R1, d.R2, d.R3, d.K0, d.L, d.C,
+                 d.contig ? "contig" : "strided", d.W, d.NT, d.smem, d.ext);
+        s += line;
+    }
+    if (buf && len) {
+        strncpy(buf, s.c_str(), len - 1);
+        buf[len - 1] = 0;
+    }
+    return PAFFT_OK;
+}
+
+// --------------------------------------------------------------- filters
+static pafft_status new_filter(pafft_plan_t p, pafft_filter_t* out) {
+    auto f = std::make_unique<pafft_filter_s>();
+    f->plan = p;
+    f->radix = p->radix;
+    f->rank = p->rank;
+    for (int q = 0; q < p->rank; ++q) f->dims[q] = p->dims[q];
+    f->prec = p->prec;
+    f->device = p->device;
+    ST_TRY(ensure(f->ghat, p->total * p->esize));
+    ST_TRY(ensure(f->ghat_scaled, p->total * p->esize));
+    *out = f.release();
+    return PAFFT_OK;
+}
+
+pafft_status pafft_filter_create_empty(pafft_plan_t p, pafft_filter_t* out) {
+    if (!p || !out) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ST_TRY(set_device(p));
+    return new_filter(p, out);
+}
+
+pafft_status pafft_filter_sync_scaled(pafft_filter_t f, void* stream) {
+    pafft_plan_t p = f->plan;
+    ST_TRY(set_device(p));
+    cudaStream_t st = (cudaStream_t)stream;
+    const double s = 1.0 / (double)p->total;
+    if (p->prec == 0)
+        scale_kernel<double><<<grid_for(p->total, 256), 256, 0, st>>>((const double2*)f->ghat->p,
+                                                                       (double2*)f->ghat_scaled->p, s, p->total);
+    else
+        scale_kernel<float><<<grid_for(p->total, 256), 256, 0, st>>>((const float2*)f->ghat->p,
+                                                                      (float2*)f->ghat_scaled->p, s, p->total);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    return PAFFT_OK;
+}
+
+pafft_status pafft_prepare_filter_device(pafft_plan_t p, const void* g_dev, void* stream, pafft_filter_t* out) {
+    if (!p || !out || !g_dev) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ST_TRY(set_device(p));
+    pafft_filter_t f;
+    ST_TRY(new_filter(p, &f));
+    std::unique_ptr<pafft_filter_s> guard(f);
+    cudaStream_t st = (cudaStream_t)stream;
+    ST_TRY(permute_dev(p, g_dev, f->ghat->p, 1, st));  // the one offline reordering pass
+    ST_TRY(pafft_filter_sync_scaled(f, stream));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    *out = guard.release();
+    return PAFFT_OK;
+}
+
+pafft_status pafft_prepare_filter_split(pafft_plan_t p, const double* g_re, const double* g_im,
+                                        pafft_filter_t* out) {
+    if (!p || !out || !g_re || !g_im) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ST_TRY(set_device(p));
+    const size_t n = p->total;
+    std::vector<double> h(2 * n);
+    for (size_t i = 0; i < n; ++i) {
+        h[2 * i] = g_re[i];
+        h[2 * i + 1] = g_im[i];
+    }
+    // the observable ghat stays bit-exact: permute in double, convert after
+    DevBuf g64, gh64;
+    CUDA_TRY(cudaMalloc(&g64.p, n * 16));
+    CUDA_TRY(cudaMalloc(&gh64.p, n * 16));
+    CUDA_TRY(cudaMemcpy(g64.p, h.data(), n * 16, cudaMemcpyHostToDevice));
+    pafft_filter_t f;
+    ST_TRY(new_filter(p, &f));
+    std::unique_ptr<pafft_filter_s> guard(f);
+    {
+        PermArgs pa;
+        memset(&pa, 0, sizeof pa);
+        pa.rank = p->rank;
+        for (int q = 0; q < p->rank; ++q) {
+            pa.dims[q] = p->dims[q];
+            pa.rev[q] = p->rev_dev[q];
+        }
+        permute_kernel<double2><<<grid_for(n, 256), 256>>>((const double2*)g64.p, (double2*)gh64.p, n, n, pa);
+        CUDA_TRY(cudaGetLastError());
+        ++g_launches;
+        ++g_perm_passes;
+    }
+    const double s = 1.0 / (double)n;
+    if (p->prec == 0)
+        scale_convert_kernel<double><<<grid_for(n, 256), 256>>>((const double2*)gh64.p, (double2*)f->ghat->p,
+                                                                (double2*)f->ghat_scaled->p, s, n);
+    else
+        scale_convert_kernel<float><<<grid_for(n, 256), 256>>>((const double2*)gh64.p, (float2*)f->ghat->p,
+                                                               (float2*)f->ghat_scaled->p, s, n);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    CUDA_TRY(cudaDeviceSynchronize());
+    *out = guard.release();
+    return PAFFT_OK;
+}
+
+pafft_status pafft_prepare_filter_from_impulse_device(pafft_plan_t p, const void* h_dev, void* stream,
+                                                      pafft_filter_t* out) {
+    if (!p || !out || !h_dev) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ST_TRY(set_device(p));
+    pafft_filter_t f;
+    ST_TRY(new_filter(p, &f));
+    std::unique_ptr<pafft_filter_s> guard(f);
+    cudaStream_t st = (cudaStream_t)stream;
+    ST_TRY(run_ladder(p, p->dif, h_dev, f->ghat->p, 1, nullptr, 1.0, st));  // ghat = A^T h, no permutation
+    ST_TRY(pafft_filter_sync_scaled(f, stream));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    *out = guard.release();
+    return PAFFT_OK;
+}
+
+pafft_status pafft_filter_destroy(pafft_filter_t f) {
+    if (!f) return PAFFT_OK;
+    cudaSetDevice(f->device);
+    delete f;
+    return PAFFT_OK;
+}
+
+pafft_status pafft_filter_ghat_split(pafft_filter_t f, double* re, double* im) {
+    if (!f) return fail(PAFFT_INVALID_ARGUMENT, "null filter");
+    pafft_plan_t p = f->plan;
+    ST_TRY(set_device(p));
+    const size_t n = p->total;
+    if (p->prec == 0) {
+        std::vector<double> h(2 * n);
+        CUDA_TRY(cudaMemcpy(h.data(), f->ghat->p, n * 16, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < n; ++i) {
+            re[i] = h[2 * i];
+            im[i] = h[2 * i + 1];
+        }
+    } else {
+        std::vector<float> h(2 * n);
+        CUDA_TRY(cudaMemcpy(h.data(), f->ghat->p, n * 8, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < n; ++i) {
+            re[i] = h[2 * i];
+            im[i] = h[2 * i + 1];
+        }
+    }
+    return PAFFT_OK;
+}
+
+void* pafft_filter_device_ghat(pafft_filter_t f) { return f ? f->ghat->p : nullptr; }
+void* pafft_filter_device_ghat_scaled(pafft_filter_t f) { return f ? f->ghat_scaled->p : nullptr; }
+
+int pafft_filter_matches(pafft_filter_t f, pafft_plan_t p) { return f && p && key_match(f, p) ? 1 : 0; }
+
+// ------------------------------------------------------------- hot path
+pafft_status pafft_convolve_permfree_oop(pafft_plan_t p, pafft_filter_t f, const void* x_dev, void* y_dev,
+                                         size_t batch, void* stream) {
+    if (!p || !f) return fail(PAFFT_INVALID_ARGUMENT, "null plan or filter");
+    if (!key_match(f, p)) return fail(PAFFT_FILTER_PLAN_MISMATCH, "prepared filter does not belong to this plan");
+    if (batch == 0) return PAFFT_OK;
+    if (!x_dev || !y_dev) return fail(PAFFT_INVALID_ARGUMENT, "null buffer");
+    ST_TRY(set_device(p));
+    cudaStream_t st = (cudaStream_t)stream;
+    const std::vector<PassDesc>& ps = p->pf;
+    if (ps.empty()) return hadamard_dev(p, x_dev, f->ghat_scaled->p, y_dev, batch, st);
+    for (size_t i = 0; i < ps.size(); ++i)
+        ST_TRY(launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch,
+                      ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr, nullptr, 1.0, st));
+    return PAFFT_OK;
+}
+
+pafft_status pafft_convolve_permfree(pafft_plan_t p, pafft_filter_t f, void* x_dev, size_t batch, void* stream) {
+    return pafft_convolve_permfree_oop(p, f, x_dev, x_dev, batch, stream);
+}
+
+static void interleave(const double* re, const double* im, size_t n, double* out) {
+    for (size_t i = 0; i < n; ++i) {
+        out[2 * i] = re[i];
+        out[2 * i + 1] = im[i];
+    }
+}
+static void deinterleave(const double* in, size_t n, double* re, double* im) {
+    for (size_t i = 0; i < n; ++i) {
+        re[i] = in[2 * i];
+        im[i] = in[2 * i + 1];
+    }
+}
+
+// host split <-> device (plan precision) helpers
+// All host<->device traffic of the split (drop-in) paths is ordered on the
+// plan's own stream; the non-blocking plan streams do not synchronise with the
+// legacy default stream, so a plain cudaMemcpy would race the kernels.
+static pafft_status upload_split(pafft_plan_t p, const double* re, const double* im, size_t n, void* dev) {
+    cudaStream_t st = p->streams[0];
+    std::vector<double> h(2 * n);
+    interleave(re, im, n, h.data());
+    if (p->prec == 0) {
+        CUDA_TRY(cudaMemcpyAsync(dev, h.data(), n * 16, cudaMemcpyHostToDevice, st));
+    } else {
+        std::vector<float> f(2 * n);
+        for (size_t i = 0; i < 2 * n; ++i) f[i] = (float)h[i];
+        CUDA_TRY(cudaMemcpyAsync(dev, f.data(), n * 8, cudaMemcpyHostToDevice, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return PAFFT_OK;
+}
+static pafft_status download_split(pafft_plan_t p, const void* dev, size_t n, double* re, double* im) {
+    cudaStream_t st = p->streams[0];
+    std::vector<double> h(2 * n);
+    if (p->prec == 0) {
+        CUDA_TRY(cudaMemcpyAsync(h.data(), dev, n * 16, cudaMemcpyDeviceToHost, st));
+    } else {
+        std::vector<float> f(2 * n);
+        CUDA_TRY(cudaMemcpyAsync(f.data(), dev, n * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        for (size_t i = 0; i < 2 * n; ++i) h[i] = f[i];
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    deinterleave(h.data(), n, re, im);
+    return PAFFT_OK;
+}
+
+pafft_status pafft_convolve_permfree_split(pafft_plan_t p, pafft_filter_t f, double* re, double* im,
+                                           size_t batch) {
+    if (!p || !f) return fail(PAFFT_INVALID_ARGUMENT, "null plan or filter");
+    if (!key_match(f, p)) return fail(PAFFT_FILTER_PLAN_MISMATCH, "prepared filter does not belong to this plan");
+    if (batch == 0) return PAFFT_OK;
+    ST_TRY(set_device(p));
+    const size_t n = p->total * batch;
+    DevBuf x;
+    CUDA_TRY(cudaMalloc(&x.p, n * p->esize));
+    ST_TRY(upload_split(p, re, im, n, x.p));
+    ST_TRY(pafft_convolve_permfree(p, f, x.p, batch, p->streams[0]));
+    CUDA_TRY(cudaStreamSynchronize(p->streams[0]));
+    return download_split(p, x.p, n, re, im);
+}
+
+pafft_status pafft_convolve_permfree_host(pafft_plan_t p, pafft_filter_t f, void* x_host, size_t batch) {
+    if (!p || !f) return fail(PAFFT_INVALID_ARGUMENT, "null plan or filter");
+    if (!key_match(f, p)) return fail(PAFFT_FILTER_PLAN_MISMATCH, "prepared filter does not belong to this plan");
+    if (batch == 0) return PAFFT_OK;
+    ST_TRY(set_device(p));
+    const size_t sig_bytes = p->total * p->esize;
+    // chunks of ~64 MiB pipelined over three streams: H2D(i+1) || conv(i) || D2H(i-1)
+    size_t chunk = std::max<size_t>(1, (size_t)(64ull << 20) / sig_bytes);
+    chunk = std::min(chunk, batch);
+    for (auto& s : p->stage) ST_TRY(ensure(s, chunk * sig_bytes));
+    char* host = (char*)x_host;
+    size_t done = 0;
+    int k = 0;
+    while (done < batch) {
+        const size_t nb = std::min(chunk, batch - done);
+        cudaStream_t st = p->streams[k % 3];
+        void* buf = p->stage[k % 3]->p;
+        CUDA_TRY(cudaMemcpyAsync(buf, host + done * sig_bytes, nb * sig_bytes, cudaMemcpyHostToDevice, st));
+        ST_TRY(pafft_convolve_permfree(p, f, buf, nb, st));
+        CUDA_TRY(cudaMemcpyAsync(host + done * sig_bytes, buf, nb * sig_bytes, cudaMemcpyDeviceToHost, st));
+        done += nb;
+        ++k;
+    }
+    for (auto& s : p->streams) CUDA_TRY(cudaStreamSynchronize(s));
+    return PAFFT_OK;
+}
+
+// ------------------------------------------------ comparator / transforms
+pafft_status pafft_permute(pafft_plan_t p, void* x, size_t batch, void* stream) {
+    if (!p) return fail(PAFFT_INVALID_ARGUMENT, "null plan");
+    ST_TRY(set_device(p));
+    cudaStream_t st = (cudaStream_t)stream;
+    ST_TRY(ensure(p->scratch, p->total * batch * p->esize));
+    ST_TRY(permute_dev(p, x, p->scratch->p, batch, st));
+    CUDA_TRY(cudaMemcpyAsync(x, p->scratch->p, p->total * batch * p->esize, cudaMemcpyDeviceToDevice, st));
+    return PAFFT_OK;
+}
+
+static pafft_status ladder_op(pafft_plan_t p, int kind, bool permute_first, double scale, const void* mul,
+                              void* x, size_t batch, cudaStream_t st) {
+    const std::vector<PassDesc>& ps = kind == KIND_DIF ? p->dif : kind == KIND_DIT_FWD ? p->dit_fwd : p->dit_conj;
+    if (permute_first) {
+        ST_TRY(ensure(p->scratch, p->total * batch * p->esize));
+        ST_TRY(permute_dev(p, x, p->scratch->p, batch, st));
+        if (ps.empty()) {
+            CUDA_TRY(cudaMemcpyAsync(x, p->scratch->p, p->total * batch * p->esize, cudaMemcpyDeviceToDevice, st));
+            if (scale != 1.0) {
+                const unsigned long long n = p->total * batch;
+                if (p->prec == 0)
+                    scale_kernel<double><<<grid_for(n, 256), 256, 0, st>>>((const double2*)x, (double2*)x, scale, n);
+                else
+                    scale_kernel<float><<<grid_for(n, 256), 256, 0, st>>>((const float2*)x, (float2*)x, scale, n);
+            }
+            return PAFFT_OK;
+        }
+        return run_ladder(p, ps, p->scratch->p, x, batch, mul, scale, st);
+    }
+    if (ps.empty() && scale != 1.0) {
+        const unsigned long long n = p->total * batch;
+        if (p->prec == 0)
+            scale_kernel<double><<<grid_for(n, 256), 256, 0, st>>>((const double2*)x, (double2*)x, scale, n);
+        else
+            scale_kernel<float><<<grid_for(n, 256), 256, 0, st>>>((const float2*)x, (float2*)x, scale, n);
+        return PAFFT_OK;
+    }
+    return run_ladder(p, ps, x, x, batch, mul, scale, st);
+}
+
+pafft_status pafft_fft_forward(pafft_plan_t p, void* x, size_t batch, void* stream) {
+    ST_TRY(set_device(p));
+    return ladder_op(p, KIND_DIT_FWD, true, 1.0, nullptr, x, batch, (cudaStream_t)stream);
+}
+pafft_status pafft_fft_backward(pafft_plan_t p, void* x, size_t batch, void* stream) {
+    ST_TRY(set_device(p));
+    return ladder_op(p, KIND_DIT_CONJ, true, 1.0 / (double)p->total, nullptr, x, batch, (cudaStream_t)stream);
+}
+pafft_status pafft_fft_forward_unordered(pafft_plan_t p, void* x, size_t batch, void* stream) {
+    ST_TRY(set_device(p));
+    return ladder_op(p, KIND_DIT_FWD, false, 1.0, nullptr, x, batch, (cudaStream_t)stream);
+}
+pafft_status pafft_fft_backward_unordered(pafft_plan_t p, void* x, size_t batch, void* stream) {
+    ST_TRY(set_device(p));
+    return ladder_op(p, KIND_DIT_CONJ, false, 1.0 / (double)p->total, nullptr, x, batch, (cudaStream_t)stream);
+}
+pafft_status pafft_fft_transposed(pafft_plan_t p, void* x, size_t batch, void* stream) {
+    ST_TRY(set_device(p));
+    return ladder_op(p, KIND_DIF, false, 1.0, nullptr, x, batch, (cudaStream_t)stream);
+}
+
+pafft_status pafft_convolve_standard(pafft_plan_t p, const void* g_dev, void* x, size_t batch, void* stream) {
+    if (!p || !g_dev) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ST_TRY(set_device(p));
+    cudaStream_t st = (cudaStream_t)stream;
+    // fft_forward (permute #1 + A), o g fused into A's last pass, fft_backward (permute #2 + A-bar + 1/N)
+    if (p->groups.empty()) {  // 1-element transform: both reorderings are identities
+        g_perm_passes += 2 * batch;
+        return hadamard_dev(p, x, g_dev, x, batch, st);
+    }
+    ST_TRY(ladder_op(p, KIND_DIT_FWD, true, 1.0, g_dev, x, batch, st));
+    ST_TRY(ladder_op(p, KIND_DIT_CONJ, true, 1.0 / (double)p->total, nullptr, x, batch, st));
+    return PAFFT_OK;
+}
+
+pafft_status pafft_convolve_standard_split(pafft_plan_t p, const double* g_re, const double* g_im, double* re,
+                                           double* im, size_t batch) {
+    if (!p) return fail(PAFFT_INVALID_ARGUMENT, "null plan");
+    if (batch == 0) return PAFFT_OK;
+    ST_TRY(set_device(p));
+    const size_t n = p->total;
+    DevBuf g, x;
+    CUDA_TRY(cudaMalloc(&g.p, n * p->esize));
+    CUDA_TRY(cudaMalloc(&x.p, n * batch * p->esize));
+    ST_TRY(upload_split(p, g_re, g_im, n, g.p));
+    ST_TRY(upload_split(p, re, im, n * batch, x.p));
+    ST_TRY(pafft_convolve_standard(p, g.p, x.p, batch, p->streams[0]));
+    CUDA_TRY(cudaStreamSynchronize(p->streams[0]));
+    return download_split(p, x.p, n * batch, re, im);
+}
+
+pafft_status pafft_transform_split(pafft_plan_t p, int op, double* re, double* im, size_t batch) {
+    if (!p) return fail(PAFFT_INVALID_ARGUMENT, "null plan");
+    if (batch == 0) return PAFFT_OK;
+    ST_TRY(set_device(p));
+    const size_t n = p->total * batch;
+    DevBuf x;
+    CUDA_TRY(cudaMalloc(&x.p, n * p->esize));
+    ST_TRY(upload_split(p, re, im, n, x.p));
+    cudaStream_t st = p->streams[0];
+    switch (op) {
+        case 0: ST_TRY(pafft_fft_forward(p, x.p, batch, st)); break;
+        case 1: ST_TRY(pafft_fft_backward(p, x.p, batch, st)); break;
+        case 2: ST_TRY(pafft_fft_forward_unordered(p, x.p, batch, st)); break;
+        case 3: ST_TRY(pafft_fft_backward_unordered(p, x.p, batch, st)); break;
+        case 4: ST_TRY(pafft_fft_transposed(p, x.p, batch, st)); break;
+        case 5: ST_TRY(pafft_permute(p, x.p, batch, st)); break;
+        default: return fail(PAFFT_INVALID_ARGUMENT, "unknown transform op %d", op);
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return download_split(p, x.p, n, re, im);
+}
+
+pafft_status pafft_filter_from_impulse_split(pafft_plan_t p, const double* h_re, const double* h_im, double* g_re,
+                                             double* g_im) {
+    if (!p) return fail(PAFFT_INVALID_ARGUMENT, "null plan");
+    memcpy(g_re, h_re, p->total * sizeof(double));
+    memcpy(g_im, h_im, p->total * sizeof(double));
+    return pafft_transform_split(p, 0, g_re, g_im, 1);
+}
+
+// ------------------------------------------------------------ workload
+static inline uint64_t splitmix64(uint64_t& s) {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+void pafft_fill_uniform(uint64_t seed, size_t n, double* out) {
+    uint64_t st = seed;
+    for (size_t i = 0; i < n; ++i) {
+        out[2 * i] = 2.0 * ((double)(splitmix64(st) >> 11) / 9007199254740991.0) - 1.0;
+        out[2 * i + 1] = 2.0 * ((double)(splitmix64(st) >> 11) / 9007199254740991.0) - 1.0;
+    }
+}
+
+void pafft_fill_normal(uint64_t seed, size_t n, double* out) {
+    uint64_t st = seed;
+    const double inv53 = 1.0 / 9007199254740992.0;
+    const double two_pi = 2.0 * 3.14159265358979323846264338327950288;
+    for (size_t i = 0; i < n; ++i) {
+        const double u1 = (double)((splitmix64(st) >> 11) + 1) * inv53;
+        const double u2 = (double)(splitmix64(st) >> 11) * inv53;
+        const double rho = sqrt(-2.0 * log(u1));
+        out[2 * i] = rho * cos(two_pi * u2);
+        out[2 * i + 1] = rho * sin(two_pi * u2);
+    }
+}
+
+}  // extern "C"
