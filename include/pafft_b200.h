@@ -109,6 +109,15 @@ pafft_status pafft_convolve_permfree(pafft_plan_t plan, pafft_filter_t filter, v
                                      void* stream);
 pafft_status pafft_convolve_permfree_oop(pafft_plan_t plan, pafft_filter_t filter, const void* x_dev,
                                          void* y_dev, size_t batch, void* stream);
+/* One pass of the same schedule (0 <= i < pafft_plan_num_passes): pass 0
+ * reads x_dev and writes y_dev, later passes work in place on y_dev.  Running
+ * i = 0..n-1 in order equals pafft_convolve_permfree_oop; used to time the
+ * passes individually with CUDA events (bench.py roofline). */
+pafft_status pafft_convolve_permfree_pass(pafft_plan_t plan, pafft_filter_t filter, const void* x_dev,
+                                          void* y_dev, size_t batch, int i, void* stream);
+/* kind: 0 DIF (A^T group), 1 DIT forward, 2 DIT conjugate, 3 fused middle
+ * (DIF + x ghat + DIT-conj); axis, R = radix^stages of the pass. */
+pafft_status pafft_plan_pass_info(pafft_plan_t plan, int i, int* kind, int* axis, int* R, int* stages);
 /* Drop-in host path: split host arrays (ComplexBuffer), synchronous, H2D and
  * D2H inside.  Mirrors convolve_permfree(ComplexBuffer&, ...) exactly. */
 pafft_status pafft_convolve_permfree_split(pafft_plan_t plan, pafft_filter_t filter, double* re, double* im,
@@ -117,6 +126,9 @@ pafft_status pafft_convolve_permfree_split(pafft_plan_t plan, pafft_filter_t fil
  * copy/compute streams; synchronous. In place on x_host. */
 pafft_status pafft_convolve_permfree_host(pafft_plan_t plan, pafft_filter_t filter, void* x_host,
                                           size_t batch);
+/* Same, out of place: reads x_host, writes y_host (bench.py e2e leg). */
+pafft_status pafft_convolve_permfree_host_oop(pafft_plan_t plan, pafft_filter_t filter, const void* x_host,
+                                              void* y_host, size_t batch);
 
 /* ------------------------------------------- comparator and transforms --
  * convolve_standard (convolution.cpp:37-43): permute, A, o g, permute,

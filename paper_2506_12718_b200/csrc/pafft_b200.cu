@@ -877,6 +877,32 @@ pafft_status pafft_convolve_permfree_oop(pafft_plan_t p, pafft_filter_t f, const
     return PAFFT_OK;
 }
 
+pafft_status pafft_convolve_permfree_pass(pafft_plan_t p, pafft_filter_t f, const void* x_dev, void* y_dev,
+                                          size_t batch, int i, void* stream) {
+    if (!p || !f) return fail(PAFFT_INVALID_ARGUMENT, "null plan or filter");
+    if (!key_match(f, p)) return fail(PAFFT_FILTER_PLAN_MISMATCH, "prepared filter does not belong to this plan");
+    const std::vector<PassDesc>& ps = p->pf;
+    if (ps.empty()) {
+        if (i != 0) return fail(PAFFT_INVALID_ARGUMENT, "pass index %d out of range", i);
+        return hadamard_dev(p, x_dev, f->ghat_scaled->p, y_dev, batch, (cudaStream_t)stream);
+    }
+    if (i < 0 || i >= (int)ps.size()) return fail(PAFFT_INVALID_ARGUMENT, "pass index %d out of range", i);
+    ST_TRY(set_device(p));
+    return launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch, ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr,
+                  nullptr, 1.0, (cudaStream_t)stream);
+}
+
+pafft_status pafft_plan_pass_info(pafft_plan_t p, int i, int* kind, int* axis, int* R, int* stages) {
+    if (!p) return fail(PAFFT_INVALID_ARGUMENT, "null plan");
+    if (i < 0 || i >= (int)p->pf.size()) return fail(PAFFT_INVALID_ARGUMENT, "pass index %d out of range", i);
+    const PassDesc& d = p->pf[i];
+    if (kind) *kind = d.kind;
+    if (axis) *axis = d.axis;
+    if (R) *R = d.R;
+    if (stages) *stages = d.s;
+    return PAFFT_OK;
+}
+
 pafft_status pafft_convolve_permfree(pafft_plan_t p, pafft_filter_t f, void* x_dev, size_t batch, void* stream) {
     return pafft_convolve_permfree_oop(p, f, x_dev, x_dev, batch, stream);
 }
@@ -943,7 +969,8 @@ pafft_status pafft_convolve_permfree_split(pafft_plan_t p, pafft_filter_t f, dou
     return download_split(p, x.p, n, re, im);
 }
 
-pafft_status pafft_convolve_permfree_host(pafft_plan_t p, pafft_filter_t f, void* x_host, size_t batch) {
+pafft_status pafft_convolve_permfree_host_oop(pafft_plan_t p, pafft_filter_t f, const void* x_host, void* y_host,
+                                              size_t batch) {
     if (!p || !f) return fail(PAFFT_INVALID_ARGUMENT, "null plan or filter");
     if (!key_match(f, p)) return fail(PAFFT_FILTER_PLAN_MISMATCH, "prepared filter does not belong to this plan");
     if (batch == 0) return PAFFT_OK;
@@ -953,21 +980,26 @@ pafft_status pafft_convolve_permfree_host(pafft_plan_t p, pafft_filter_t f, void
     size_t chunk = std::max<size_t>(1, (size_t)(64ull << 20) / sig_bytes);
     chunk = std::min(chunk, batch);
     for (auto& s : p->stage) ST_TRY(ensure(s, chunk * sig_bytes));
-    char* host = (char*)x_host;
+    const char* src = (const char*)x_host;
+    char* dst = (char*)y_host;
     size_t done = 0;
     int k = 0;
     while (done < batch) {
         const size_t nb = std::min(chunk, batch - done);
         cudaStream_t st = p->streams[k % 3];
         void* buf = p->stage[k % 3]->p;
-        CUDA_TRY(cudaMemcpyAsync(buf, host + done * sig_bytes, nb * sig_bytes, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(buf, src + done * sig_bytes, nb * sig_bytes, cudaMemcpyHostToDevice, st));
         ST_TRY(pafft_convolve_permfree(p, f, buf, nb, st));
-        CUDA_TRY(cudaMemcpyAsync(host + done * sig_bytes, buf, nb * sig_bytes, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(dst + done * sig_bytes, buf, nb * sig_bytes, cudaMemcpyDeviceToHost, st));
         done += nb;
         ++k;
     }
     for (auto& s : p->streams) CUDA_TRY(cudaStreamSynchronize(s));
     return PAFFT_OK;
+}
+
+pafft_status pafft_convolve_permfree_host(pafft_plan_t p, pafft_filter_t f, void* x_host, size_t batch) {
+    return pafft_convolve_permfree_host_oop(p, f, x_host, x_host, batch);
 }
 
 // ------------------------------------------------ comparator / transforms
