@@ -82,78 +82,91 @@ template <int P, int E, int S, typename V> __device__ __forceinline__ V twiddle_
     }
 }
 
+// Codelets work in place on a register array z at compile-time positions
+// z[OFF + i*ST], i < P: input index i, output frequency k left at
+// z[OFF + pos(k)*ST].  Primitive sizes have pos(k) = k; composite sizes keep
+// their sub-results where they were computed (no transposition moves), so the
+// live register set stays ~P complex values.
 template <int P, int S> struct Dft;
 
 template <int S> struct Dft<1, S> {
-    template <typename V> static __device__ __forceinline__ void run(V (&)[1]) {}
+    static constexpr int pos(int k) { return k; }
+    template <int ST, int OFF, typename V, int N> static __device__ __forceinline__ void run(V (&)[N]) {}
 };
 
 template <int S> struct Dft<2, S> {
-    template <typename V> static __device__ __forceinline__ void run(V (&z)[2]) {
-        const V a = z[0], b = z[1];
-        z[0] = cadd(a, b);
-        z[1] = csub(a, b);
+    static constexpr int pos(int k) { return k; }
+    template <int ST, int OFF, typename V, int N> static __device__ __forceinline__ void run(V (&z)[N]) {
+        const V a = z[OFF], b = z[OFF + ST];
+        z[OFF] = cadd(a, b);
+        z[OFF + ST] = csub(a, b);
     }
 };
 
 template <int S> struct Dft<3, S> {
-    template <typename V> static __device__ __forceinline__ void run(V (&z)[3]) {
+    static constexpr int pos(int k) { return k; }
+    template <int ST, int OFF, typename V, int N> static __device__ __forceinline__ void run(V (&z)[N]) {
         using T = decltype(z[0].x);
         const T s = (T)(S * PAFFT_SIN60);
-        const V t1 = cadd(z[1], z[2]);
-        const V t2 = csub(z[1], z[2]);
-        const V m{z[0].x - (T)0.5 * t1.x, z[0].y - (T)0.5 * t1.y};
-        z[0] = cadd(z[0], t1);
-        z[1] = V{m.x + s * t2.y, m.y - s * t2.x};
-        z[2] = V{m.x - s * t2.y, m.y + s * t2.x};
+        const V a = z[OFF];
+        const V t1 = cadd(z[OFF + ST], z[OFF + 2 * ST]);
+        const V t2 = csub(z[OFF + ST], z[OFF + 2 * ST]);
+        const V m{a.x - (T)0.5 * t1.x, a.y - (T)0.5 * t1.y};
+        z[OFF] = cadd(a, t1);
+        z[OFF + ST] = V{m.x + s * t2.y, m.y - s * t2.x};
+        z[OFF + 2 * ST] = V{m.x - s * t2.y, m.y + s * t2.x};
     }
 };
 
 template <int S> struct Dft<4, S> {
-    template <typename V> static __device__ __forceinline__ void run(V (&z)[4]) {
-        const V t0 = cadd(z[0], z[2]), t1 = csub(z[0], z[2]);
-        const V t2 = cadd(z[1], z[3]), t3 = rot_mi<S>(csub(z[1], z[3]));
-        z[0] = cadd(t0, t2);
-        z[2] = csub(t0, t2);
-        z[1] = cadd(t1, t3);
-        z[3] = csub(t1, t3);
+    static constexpr int pos(int k) { return k; }
+    template <int ST, int OFF, typename V, int N> static __device__ __forceinline__ void run(V (&z)[N]) {
+        const V t0 = cadd(z[OFF], z[OFF + 2 * ST]), t1 = csub(z[OFF], z[OFF + 2 * ST]);
+        const V t2 = cadd(z[OFF + ST], z[OFF + 3 * ST]);
+        const V t3 = rot_mi<S>(csub(z[OFF + ST], z[OFF + 3 * ST]));
+        z[OFF] = cadd(t0, t2);
+        z[OFF + 2 * ST] = csub(t0, t2);
+        z[OFF + ST] = cadd(t1, t3);
+        z[OFF + 3 * ST] = csub(t1, t3);
     }
 };
 
 template <int S> struct Dft<5, S> {
-    template <typename V> static __device__ __forceinline__ void run(V (&z)[5]) {
+    static constexpr int pos(int k) { return k; }
+    template <int ST, int OFF, typename V, int N> static __device__ __forceinline__ void run(V (&z)[N]) {
         using T = decltype(z[0].x);
         const T c1 = (T)PAFFT_C51, c2 = (T)PAFFT_C52;
         const T s1 = (T)(S * PAFFT_S51), s2 = (T)(S * PAFFT_S52);
-        const V t1 = cadd(z[1], z[4]), t2 = cadd(z[2], z[3]);
-        const V t3 = csub(z[1], z[4]), t4 = csub(z[2], z[3]);
-        const V a = z[0];
+        const V a = z[OFF];
+        const V t1 = cadd(z[OFF + ST], z[OFF + 4 * ST]), t2 = cadd(z[OFF + 2 * ST], z[OFF + 3 * ST]);
+        const V t3 = csub(z[OFF + ST], z[OFF + 4 * ST]), t4 = csub(z[OFF + 2 * ST], z[OFF + 3 * ST]);
         const V m1{a.x + c1 * t1.x + c2 * t2.x, a.y + c1 * t1.y + c2 * t2.y};
         const V m2{a.x + c2 * t1.x + c1 * t2.x, a.y + c2 * t1.y + c1 * t2.y};
         const V n1{s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y};
         const V n2{s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y};
-        z[0] = V{a.x + t1.x + t2.x, a.y + t1.y + t2.y};
+        z[OFF] = V{a.x + t1.x + t2.x, a.y + t1.y + t2.y};
         // Z1 = m1 - i n1, Z4 = m1 + i n1, Z2 = m2 - i n2, Z3 = m2 + i n2
-        z[1] = V{m1.x + n1.y, m1.y - n1.x};
-        z[4] = V{m1.x - n1.y, m1.y + n1.x};
-        z[2] = V{m2.x + n2.y, m2.y - n2.x};
-        z[3] = V{m2.x - n2.y, m2.y + n2.x};
+        z[OFF + ST] = V{m1.x + n1.y, m1.y - n1.x};
+        z[OFF + 4 * ST] = V{m1.x - n1.y, m1.y + n1.x};
+        z[OFF + 2 * ST] = V{m2.x + n2.y, m2.y - n2.x};
+        z[OFF + 3 * ST] = V{m2.x - n2.y, m2.y + n2.x};
     }
 };
 
 template <int S> struct Dft<8, S> {
-    template <typename V> static __device__ __forceinline__ void run(V (&z)[8]) {
-        V e[4] = {z[0], z[2], z[4], z[6]};
-        V o[4] = {z[1], z[3], z[5], z[7]};
-        Dft<4, S>::run(e);
-        Dft<4, S>::run(o);
+    static constexpr int pos(int k) { return k; }
+    template <int ST, int OFF, typename V, int N> static __device__ __forceinline__ void run(V (&z)[N]) {
+        V e[4] = {z[OFF], z[OFF + 2 * ST], z[OFF + 4 * ST], z[OFF + 6 * ST]};
+        V o[4] = {z[OFF + ST], z[OFF + 3 * ST], z[OFF + 5 * ST], z[OFF + 7 * ST]};
+        Dft<4, S>::template run<1, 0>(e);
+        Dft<4, S>::template run<1, 0>(o);
         o[1] = rot8<1, S>(o[1]);
         o[2] = rot8<2, S>(o[2]);
         o[3] = rot8<3, S>(o[3]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            z[k] = cadd(e[k], o[k]);
-            z[k + 4] = csub(e[k], o[k]);
+            z[OFF + k * ST] = cadd(e[k], o[k]);
+            z[OFF + (k + 4) * ST] = csub(e[k], o[k]);
         }
     }
 };
@@ -169,34 +182,43 @@ template <> struct Split<64> { static constexpr int A = 8; };
 template <> struct Split<81> { static constexpr int A = 9; };
 template <> struct Split<125> { static constexpr int A = 5; };
 
+// In-place Cooley-Tukey: index m = m1*B + m2, frequency k = k1 + A*k2.
+//   (1) for each column m2: A-point DFT over m1 (stride B), in place;
+//       twiddle the result for k1 by w_P^{m2 k1};
+//   (2) for each k1 (row at A-position pos_A(k1)): B-point DFT over m2.
+// Frequency k1 + A k2 ends at pos_A(k1) * B + pos_B(k2).
 template <int P, int S> struct Dft {
     static constexpr int A = Split<P>::A;
     static constexpr int B = P / A;
-    // m = m1*B + m2, k = k1 + A*k2:
-    // Z[k1 + A k2] = sum_m2 w_B^{m2 k2} [ w_P^{m2 k1} sum_m1 w_A^{m1 k1} z[m1 B + m2] ]
-    template <typename V> static __device__ __forceinline__ void run(V (&z)[P]) {
-        V v[P];
+    static constexpr int pos(int k) { return Dft<A, S>::pos(k % A) * B + Dft<B, S>::pos(k / A); }
+    template <int ST, int OFF, typename V, int N> static __device__ __forceinline__ void run(V (&z)[N]) {
         static_for<0, B>([&](auto m2c) {
             constexpr int m2 = decltype(m2c)::value;
-            V u[A];
-#pragma unroll
-            for (int m1 = 0; m1 < A; ++m1) u[m1] = z[m1 * B + m2];
-            Dft<A, S>::run(u);
-            static_for<0, A>([&](auto k1c) {
+            Dft<A, S>::template run<ST * B, OFF + m2 * ST>(z);
+            static_for<1, A>([&](auto k1c) {
                 constexpr int k1 = decltype(k1c)::value;
-                v[k1 * B + m2] = twiddle_const<P, k1 * m2, S>(u[k1]);
+                constexpr int slot = OFF + (Dft<A, S>::pos(k1) * B + m2) * ST;
+                z[slot] = twiddle_const<P, k1 * m2, S>(z[slot]);
             });
         });
-#pragma unroll
-        for (int k1 = 0; k1 < A; ++k1) {
-            V t[B];
-#pragma unroll
-            for (int m2 = 0; m2 < B; ++m2) t[m2] = v[k1 * B + m2];
-            Dft<B, S>::run(t);
-#pragma unroll
-            for (int k2 = 0; k2 < B; ++k2) z[k1 + A * k2] = t[k2];
-        }
+        static_for<0, A>([&](auto k1c) {
+            constexpr int k1 = decltype(k1c)::value;
+            Dft<B, S>::template run<ST, OFF + Dft<A, S>::pos(k1) * B * ST>(z);
+        });
     }
 };
+
+// Whole-array transform with natural-order result (z[k] = frequency k): the
+// in-place codelet followed by a compile-time renaming (no data movement).
+template <int P, int S, typename V> __device__ __forceinline__ void dft(V (&z)[P]) {
+    Dft<P, S>::template run<1, 0>(z);
+    if constexpr (P > 1) {
+        V w[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) w[k] = z[Dft<P, S>::pos(k)];
+#pragma unroll
+        for (int k = 0; k < P; ++k) z[k] = w[k];
+    }
+}
 
 }  // namespace pafft_b200

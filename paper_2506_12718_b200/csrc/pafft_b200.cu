@@ -77,9 +77,9 @@ Registry& registry() {
     return reg;
 }
 
-const KernelEntry* find_kernel(int prec, int radix, int R, int kind) {
+const KernelEntry* find_kernel(int prec, int radix, int R, int kind, int map) {
     for (const auto& e : registry())
-        if (e.prec == prec && e.radix == radix && e.R == R && e.kind == kind) return &e;
+        if (e.prec == prec && e.radix == radix && e.R == R && e.kind == kind && e.map == map) return &e;
     return nullptr;
 }
 
@@ -272,12 +272,12 @@ void build_groups(pafft_plan_t p) {
         if (q == 0 && t > max_mid) {
             // outer strided groups, then the contiguous group (gets the remainder)
             const int npass = (t + std::min(max_mid, max_str) - 1) / std::min(max_mid, max_str);
-            int rem = t, a = 0;
+            int a = 0;
             for (int i = 0; i < npass; ++i) {
-                const int s = (rem + (npass - i) - 1) / (npass - i);
+                // even split, remainder to the last (contiguous, CONV) groups
+                const int s = t / npass + (i >= npass - t % npass ? 1 : 0);
                 p->groups.push_back({q, a, s});
                 a += s;
-                rem -= s;
             }
         } else {
             const int npass = (t + lim - 1) / lim;
@@ -309,31 +309,18 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     d.sq = sq;
     d.C = d.L * sq;
     d.contig = d.C == 1;
-    const KernelEntry* ke = find_kernel(p->prec, (int)p->radix, d.R, kind);
-    if (!ke) return fail(PAFFT_INVALID_ARGUMENT, "no kernel for radix %u R=%d kind %d", p->radix, d.R, kind);
+    const KernelEntry* ke = find_kernel(p->prec, (int)p->radix, d.R, kind, d.contig ? MAP_CONTIG : MAP_STRIDED);
+    if (!ke)
+        return fail(PAFFT_INVALID_ARGUMENT, "no kernel for radix %u R=%d kind %d map %d", p->radix, d.R, kind,
+                    d.contig);
     d.fn = ke->fn;
     d.R1 = ke->R1;
     d.R2 = ke->R2;
     d.R3 = ke->R3;
+    d.W = ke->W;
+    d.NT = ke->NT;
+    d.smem = (size_t)ke->smem;
     const int nstep = 1 + (d.R2 > 1) + (d.R3 > 1);
-    int gmax = d.R / d.R1;
-    if (d.R2 > 1) gmax = std::max(gmax, d.R / d.R2);
-    if (d.R3 > 1) gmax = std::max(gmax, d.R / d.R3);
-    const size_t budget = (size_t)env_int("PAFFT_SMEM_BUDGET", 110 * 1024);
-    const size_t col_bytes = (size_t)d.R * p->esize;
-    if (d.contig) {
-        int W = std::max(1, 256 / std::max(gmax, 1));
-        if (nstep > 1) W = (int)std::max<size_t>(1, std::min<size_t>(W, budget / col_bytes));
-        d.W = W;
-    } else {
-        int W = p->prec == 0 ? 8 : 16;
-        W = env_int("PAFFT_STRIDED_W", W);
-        if (nstep > 1) W = (int)std::max<size_t>(1, std::min<size_t>(W, budget / col_bytes));
-        d.W = (int)std::min<long long>(W, d.C);
-    }
-    const int work = gmax * d.W;
-    d.NT = std::min(256, std::max(32, (work + 31) / 32 * 32));
-    d.smem = nstep > 1 ? (size_t)d.R * d.W * p->esize : 0;
     if (d.smem > 48 * 1024)
         CUDA_TRY(cudaFuncSetAttribute(d.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
     d.ext = d.L > 1;
@@ -353,8 +340,6 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     a.panels = per_signal * (long long)batch;
     a.panel_elems = (long long)d.R * d.C;
     a.C = (int)d.C;
-    a.W = d.W;
-    a.contig = d.contig;
     a.tiles_per_panel = d.contig ? 1 : (int)((d.C + d.W - 1) / d.W);
     a.tiles = d.contig ? (a.panels + d.W - 1) / d.W : a.panels * a.tiles_per_panel;
     a.ext = d.ext;

@@ -18,10 +18,18 @@
 //
 // Inside a tile the R-point column transform is R = R1 * R2 * R3 with
 // in-register codelets (codelets.cuh) and shared-memory exchanges between
-// steps (four-step decomposition with internal twiddles w_R, w_{R2 R3} from
-// L1-resident tables laid out for the access pattern).  Each codelet size is a
-// power of r, so rev(k) splits per step.  Layout is interleaved complex
-// (double2 / float2): every element is one 16-byte (8-byte) vector access.
+// steps (four-step decomposition; internal twiddles w_R, w_{R2 R3} from
+// L1-resident tables laid out for the access pattern; the external twiddle
+// w_K0^{jj k} by a per-thread recurrence from a two-level table).  Each codelet
+// size is a power of r, so rev(k) splits per step.
+//
+// Tile geometry is compile-time: W columns (STRIDED map: W adjacent columns
+// of one panel, so every row segment is a W*16-byte coalesced run and each
+// shared-memory row is conflict-free) or W panels (CONTIG map: C == 1, W
+// consecutive contiguous blocks).  Every thread owns one (column, group-slot)
+// pair; step i handles G_i / GMIN groups per thread at compile-time offsets,
+// so all shared/global index arithmetic folds to per-thread bases plus
+// immediates.  Layout is interleaved complex (double2 / float2).
 #pragma once
 
 #include "codelets.cuh"
@@ -29,6 +37,7 @@
 namespace pafft_b200 {
 
 enum PassKind : int { KIND_DIF = 0, KIND_DIT_FWD = 1, KIND_DIT_CONJ = 2, KIND_CONV = 3 };
+enum PassMap : int { MAP_STRIDED = 0, MAP_CONTIG = 1 };
 
 template <typename T> struct PassArgs {
     const cplx<T>* src;
@@ -37,8 +46,6 @@ template <typename T> struct PassArgs {
     long long panels;        // total panels over the batch
     long long panel_elems;   // R * C
     int C;                   // columns per panel (contiguous)
-    int W;                   // tile width: columns (strided) or panels (contig)
-    int contig;              // 1: C == 1, tile = W consecutive panels
     int tiles_per_panel;     // ceil(C / W) for strided tiles
     // external twiddle w_K0^{jj k}, jj = column / sq, two-level table
     int ext;
@@ -59,15 +66,52 @@ template <typename T> struct PassArgs {
 };
 
 // Base-r digit reversal over the digits of P = r^s (permutation.cpp:27-37).
-template <int RADIX, int P> __device__ __forceinline__ int revd(int k) {
+template <int RADIX, int P> __host__ __device__ constexpr int revd(int k) {
     int o = 0;
-#pragma unroll
     for (int p = 1; p < P; p *= RADIX) {
         o = o * RADIX + k % RADIX;
         k /= RADIX;
     }
     return o;
 }
+
+template <int R1, int R2, int R3> struct Shape {
+    static constexpr int R = R1 * R2 * R3;
+    static constexpr int R23 = R2 * R3;
+    static constexpr int NSTEP = 1 + (R2 > 1 ? 1 : 0) + (R3 > 1 ? 1 : 0);
+    static constexpr int G1 = R23;       // step 1 groups: m23
+    static constexpr int G2 = R1 * R3;   // step 2 groups: (k1, m3)
+    static constexpr int G3 = R1 * R2;   // step 3 groups: (k1, k2)
+    static constexpr int gmin() {
+        int g = G1;
+        if (NSTEP >= 2 && G2 < g) g = G2;
+        if (NSTEP == 3 && G3 < g) g = G3;
+        return g;
+    }
+    static constexpr int GMIN = gmin();
+};
+
+// Compile-time tile policy shared by kernels and host plan (registry).
+template <typename T, int R1, int R2, int R3, int MAP> struct TilePolicy {
+    using S = Shape<R1, R2, R3>;
+    static constexpr int ESZ = (int)sizeof(cplx<T>);
+    static constexpr int SMEM_BUDGET = 112 * 1024;
+    // STRIDED: 8 (fp64) / 16 (fp32) columns = one 128-byte row segment; more
+    // columns for single-codelet passes (no shared memory, tiny groups).
+    static constexpr int MAXW = MAP == MAP_STRIDED ? (S::NSTEP == 1 ? 64 : (ESZ == 16 ? 8 : 16)) : 64;
+    static constexpr int wcalc() {
+        int w = MAXW;
+        while (w > 1 && S::GMIN * w > 512) --w;
+        if (MAP == MAP_CONTIG)
+            while (w > 1 && S::GMIN * w > 256) --w;
+        if (S::NSTEP > 1)
+            while (w > 1 && S::R * w * ESZ > SMEM_BUDGET) --w;
+        return w;
+    }
+    static constexpr int W = wcalc();
+    static constexpr int NT = S::GMIN * W;
+    static constexpr int SMEM = S::NSTEP > 1 ? S::R * W * ESZ : 0;
+};
 
 template <typename T>
 __device__ __forceinline__ cplx<T> ext_root(const PassArgs<T>& a, unsigned long long e) {
@@ -76,183 +120,176 @@ __device__ __forceinline__ cplx<T> ext_root(const PassArgs<T>& a, unsigned long 
     return cmul(lo, hi);
 }
 
-template <typename T, int RADIX, int R1, int R2, int R3, int KIND>
-__global__ void __launch_bounds__(256) pass_kernel(PassArgs<T> a) {
+template <typename T, int RADIX, int R1, int R2, int R3, int KIND, int MAP>
+__global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
+    pass_kernel(const PassArgs<T> a) {
     using V = cplx<T>;
-    constexpr int R = R1 * R2 * R3;
-    constexpr int R23 = R2 * R3;
-    constexpr int NSTEP = 1 + (R2 > 1 ? 1 : 0) + (R3 > 1 ? 1 : 0);
-    static_assert(R3 == 1 || R2 > 1, "R3 > 1 requires R2 > 1");
+    using Sh = Shape<R1, R2, R3>;
+    using Pol = TilePolicy<T, R1, R2, R3, MAP>;
+    constexpr int R = Sh::R, R23 = Sh::R23, NSTEP = Sh::NSTEP, GMIN = Sh::GMIN;
+    constexpr int W = Pol::W;
+    constexpr bool STRIDED = MAP == MAP_STRIDED;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    V* sm = reinterpret_cast<V*>(smem_raw);
+    V* const sm = reinterpret_cast<V*>(smem_raw);
 
-    const int W = a.W;
-    const int NT = blockDim.x;
-    const int tid = threadIdx.x;
-    const bool contig = a.contig != 0;
+    const int t = threadIdx.x;
+    // thread -> (tile column c, group slot gt); STRIDED: c fastest (coalesced
+    // W-wide row segments, conflict-free smem rows); CONTIG: group fastest.
+    const int c = STRIDED ? t % W : t / GMIN;
+    const int gt = STRIDED ? t / W : t % GMIN;
+    // shared element (j, c): STRIDED sm[j*W + c], CONTIG sm[c*R + j]
+    V* const scol = STRIDED ? sm + c : sm + c * R;
+    constexpr int SS = STRIDED ? W : 1;  // shared stride between consecutive j
 
     for (long long tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
-        // ---- tile geometry: element (row m, tile column c) at base + m*rs + c*cs
-        long long base, first;  // first: first panel (contig) or column (strided)
+        long long base, first;
         int nvalid;
-        long long rs, cs;
-        if (contig) {
+        if (!STRIDED) {
             first = tile * W;
             const long long left = a.panels - first;
             nvalid = left < W ? (int)left : W;
-            base = first * (long long)R;
-            rs = 1;
-            cs = R;
+            base = first * (long long)R + (long long)c * R;
         } else {
             const long long p = tile / a.tiles_per_panel;
             first = (tile - p * a.tiles_per_panel) * (long long)W;
             const long long left = a.C - first;
             nvalid = left < W ? (int)left : W;
-            base = p * a.panel_elems + first;
-            rs = a.C;
-            cs = 1;
+            base = p * a.panel_elems + first + c;
         }
-        const V* __restrict__ src = a.src;
-        V* __restrict__ dst = a.dst;
-        auto sidx = [&](int j, int c) -> int { return contig ? c * R + j : j * W + c; };
-        auto item = [&](int w, int G, int& g, int& c) {
-            if (contig) { g = w % G; c = w / G; }
-            else { c = w % W; g = w / W; }
-        };
-        // external twiddle base/step for column c: w_K0^{jj kf}, w_K0^{jj S}
-        auto ext_pair = [&](int c, int kf, int S, V& t, V& s) {
-            const unsigned long long col = (unsigned long long)(first + c);
-            const unsigned long long jj = col / a.sq;
-            t = ext_root(a, jj * (unsigned long long)kf);
-            s = ext_root(a, jj * (unsigned long long)S);
+        const bool ok = c < nvalid;
+        const long long rs = STRIDED ? (long long)a.C : 1;  // global row stride
+        const V* __restrict__ gsrc = a.src + base;
+        V* __restrict__ gdst = a.dst + base;
+        // external twiddle base/step for this column: w_K0^{jj kf}, w_K0^{jj S}
+        auto ext_pair = [&](int kf, int S, V& tw, V& st) {
+            const unsigned long long jj = (unsigned long long)(first + c) / a.sq;
+            tw = ext_root(a, jj * (unsigned long long)kf);
+            st = ext_root(a, jj * (unsigned long long)S);
         };
 
         if constexpr (KIND == KIND_DIF || KIND == KIND_CONV) {
             // ------------------------------------------------ DIF step 1
-            {
-                constexpr int G = R23;
-                for (int w = tid; w < G * W; w += NT) {
-                    int g, c;
-                    item(w, G, g, c);
-                    const bool ok = c < nvalid;
-                    V z[R1];
 #pragma unroll
-                    for (int m1 = 0; m1 < R1; ++m1)
-                        z[m1] = ok ? src[base + (long long)(m1 * R23 + g) * rs + c * cs] : V{0, 0};
-                    Dft<R1, 1>::run(z);
-                    if constexpr (NSTEP == 1) {
-                        if constexpr (KIND == KIND_DIF) {
-                            if (ok) {
-                                V t{1, 0}, s{1, 0};
-                                if (a.ext) ext_pair(c, 0, 1, t, s);
+            for (int j = 0; j < Sh::G1 / GMIN; ++j) {
+                const int g = gt + j * GMIN;  // m23
+                V z[R1];
 #pragma unroll
-                                for (int k1 = 0; k1 < R1; ++k1) {
-                                    const V y = a.ext ? cmul(z[k1], t) : z[k1];
-                                    dst[base + (long long)revd<RADIX, R1>(k1) * rs + c * cs] = y;
-                                    if (a.ext) t = cmul(t, s);
-                                }
-                            }
-                        } else {  // CONV with a single codelet: x ghat, inverse, store
-                            if (ok) {
-                                const long long gofs = ((first + c) % (a.N / R)) * (long long)R;
+                for (int m1 = 0; m1 < R1; ++m1)
+                    z[m1] = ok ? gsrc[(long long)(m1 * R23 + g) * rs] : V{0, 0};
+                dft<R1, 1>(z);
+                if constexpr (NSTEP == 1) {
+                    if constexpr (KIND == KIND_DIF) {
+                        if (ok) {
+                            V tw{1, 0}, st{1, 0};
+                            if (a.ext) ext_pair(0, 1, tw, st);
 #pragma unroll
-                                for (int k1 = 0; k1 < R1; ++k1)
-                                    z[k1] = cmul(z[k1], __ldg(a.ghat + gofs + revd<RADIX, R1>(k1)));
-                                Dft<R1, -1>::run(z);
-#pragma unroll
-                                for (int m1 = 0; m1 < R1; ++m1) dst[base + (long long)m1 * rs + c * cs] = z[m1];
+                            for (int k1 = 0; k1 < R1; ++k1) {
+                                gdst[(long long)revd<RADIX, R1>(k1) * rs] = a.ext ? cmul(z[k1], tw) : z[k1];
+                                if (a.ext) tw = cmul(tw, st);
                             }
                         }
-                    } else {
+                    } else {  // CONV with a single codelet: x ghat, inverse, store
+                        if (ok) {
+                            const V* gh = a.ghat + ((first + c) % (a.N / R)) * (long long)R;
 #pragma unroll
-                        for (int k1 = 1; k1 < R1; ++k1) z[k1] = cmul(z[k1], __ldg(a.tw1 + k1 * R23 + g));
+                            for (int k1 = 0; k1 < R1; ++k1) z[k1] = cmul(z[k1], __ldg(gh + revd<RADIX, R1>(k1)));
+                            dft<R1, -1>(z);
 #pragma unroll
-                        for (int k1 = 0; k1 < R1; ++k1) sm[sidx(k1 * R23 + g, c)] = z[k1];
+                            for (int m1 = 0; m1 < R1; ++m1) gdst[(long long)m1 * rs] = z[m1];
+                        }
                     }
+                } else {
+                    const V* tw1 = a.tw1 + g;
+#pragma unroll
+                    for (int k1 = 1; k1 < R1; ++k1) z[k1] = cmul(z[k1], __ldg(tw1 + k1 * R23));
+#pragma unroll
+                    for (int k1 = 0; k1 < R1; ++k1) scol[(k1 * R23 + g) * SS] = z[k1];
                 }
             }
             if constexpr (NSTEP >= 2) {
                 __syncthreads();
                 // -------------------------------------------- DIF step 2
-                constexpr int G = R1 * R3;
-                for (int w = tid; w < G * W; w += NT) {
-                    int g, c;
-                    item(w, G, g, c);
+#pragma unroll
+                for (int j = 0; j < Sh::G2 / GMIN; ++j) {
+                    const int g = gt + j * GMIN;
                     const int k1 = g / R3, m3 = g - (g / R3) * R3;
+                    V* sp = scol + (k1 * R23 + m3) * SS;
                     V z[R2];
 #pragma unroll
-                    for (int m2 = 0; m2 < R2; ++m2) z[m2] = sm[sidx(k1 * R23 + m2 * R3 + m3, c)];
-                    Dft<R2, 1>::run(z);
+                    for (int m2 = 0; m2 < R2; ++m2) z[m2] = sp[m2 * R3 * SS];
+                    dft<R2, 1>(z);
                     if constexpr (NSTEP == 2) {
-                        const bool ok = c < nvalid;
                         const int pfix = revd<RADIX, R1>(k1) * R23;
                         if constexpr (KIND == KIND_DIF) {
                             if (ok) {
-                                V t{1, 0}, s{1, 0};
-                                if (a.ext) ext_pair(c, k1, R1, t, s);
+                                V tw{1, 0}, st{1, 0};
+                                if (a.ext) ext_pair(k1, R1, tw, st);
 #pragma unroll
                                 for (int k2 = 0; k2 < R2; ++k2) {
-                                    const V y = a.ext ? cmul(z[k2], t) : z[k2];
-                                    dst[base + (long long)(pfix + revd<RADIX, R2>(k2)) * rs + c * cs] = y;
-                                    if (a.ext) t = cmul(t, s);
+                                    gdst[(long long)(pfix + revd<RADIX, R2>(k2)) * rs] = a.ext ? cmul(z[k2], tw) : z[k2];
+                                    if (a.ext) tw = cmul(tw, st);
                                 }
                             }
-                        } else {  // CONV: x ghat, DIT-conj step B, back to smem
-                            const long long gofs = ok ? ((first + c) % (a.N / R)) * (long long)R : 0;
+                        } else {  // CONV: x ghat, DIT-conj step B (in registers), back to smem
+                            if (ok) {
+                                const V* gh = a.ghat + ((first + c) % (a.N / R)) * (long long)R + pfix;
 #pragma unroll
-                            for (int k2 = 0; k2 < R2; ++k2)
-                                z[k2] = cmul(z[k2], __ldg(a.ghat + gofs + pfix + revd<RADIX, R2>(k2)));
-                            Dft<R2, -1>::run(z);
+                                for (int k2 = 0; k2 < R2; ++k2) z[k2] = cmul(z[k2], __ldg(gh + revd<RADIX, R2>(k2)));
+                            }
+                            dft<R2, -1>(z);
+                            const V* tw1 = a.tw1 + k1 * R23;
 #pragma unroll
-                            for (int m2 = 1; m2 < R2; ++m2) z[m2] = cmulc(z[m2], __ldg(a.tw1 + k1 * R23 + m2));
+                            for (int m2 = 1; m2 < R2; ++m2) z[m2] = cmulc(z[m2], __ldg(tw1 + m2));
 #pragma unroll
-                            for (int m2 = 0; m2 < R2; ++m2) sm[sidx(k1 * R23 + m2, c)] = z[m2];
+                            for (int m2 = 0; m2 < R2; ++m2) sp[m2 * SS] = z[m2];
                         }
                     } else {
+                        const V* tw2 = a.tw2 + m3;
 #pragma unroll
-                        for (int k2 = 1; k2 < R2; ++k2) z[k2] = cmul(z[k2], __ldg(a.tw2 + k2 * R3 + m3));
+                        for (int k2 = 1; k2 < R2; ++k2) z[k2] = cmul(z[k2], __ldg(tw2 + k2 * R3));
 #pragma unroll
-                        for (int k2 = 0; k2 < R2; ++k2) sm[sidx(k1 * R23 + k2 * R3 + m3, c)] = z[k2];
+                        for (int k2 = 0; k2 < R2; ++k2) sp[k2 * R3 * SS] = z[k2];
                     }
                 }
             }
             if constexpr (NSTEP == 3) {
                 __syncthreads();
                 // -------------------------------------------- DIF step 3
-                constexpr int G = R1 * R2;
-                for (int w = tid; w < G * W; w += NT) {
-                    int g, c;
-                    item(w, G, g, c);
+#pragma unroll
+                for (int j = 0; j < Sh::G3 / GMIN; ++j) {
+                    const int g = gt + j * GMIN;
                     const int k1 = g / R2, k2 = g - (g / R2) * R2;
-                    const bool ok = c < nvalid;
+                    V* sp = scol + (k1 * R23 + k2 * R3) * SS;
                     V z[R3];
 #pragma unroll
-                    for (int m3 = 0; m3 < R3; ++m3) z[m3] = sm[sidx(k1 * R23 + k2 * R3 + m3, c)];
-                    Dft<R3, 1>::run(z);
+                    for (int m3 = 0; m3 < R3; ++m3) z[m3] = sp[m3 * SS];
+                    dft<R3, 1>(z);
                     const int pfix = revd<RADIX, R1>(k1) * R23 + revd<RADIX, R2>(k2) * R3;
                     if constexpr (KIND == KIND_DIF) {
                         if (ok) {
-                            V t{1, 0}, s{1, 0};
-                            if (a.ext) ext_pair(c, k1 + R1 * k2, R1 * R2, t, s);
+                            V tw{1, 0}, st{1, 0};
+                            if (a.ext) ext_pair(k1 + R1 * k2, R1 * R2, tw, st);
+                            V* gp = gdst + (long long)pfix * rs;
 #pragma unroll
                             for (int k3 = 0; k3 < R3; ++k3) {
-                                const V y = a.ext ? cmul(z[k3], t) : z[k3];
-                                dst[base + (long long)(pfix + revd<RADIX, R3>(k3)) * rs + c * cs] = y;
-                                if (a.ext) t = cmul(t, s);
+                                gp[(long long)revd<RADIX, R3>(k3) * rs] = a.ext ? cmul(z[k3], tw) : z[k3];
+                                if (a.ext) tw = cmul(tw, st);
                             }
                         }
                     } else {  // CONV: x ghat, DIT-conj step A
-                        const long long gofs = ok ? ((first + c) % (a.N / R)) * (long long)R : 0;
+                        if (ok) {
+                            const V* gh = a.ghat + ((first + c) % (a.N / R)) * (long long)R + pfix;
 #pragma unroll
-                        for (int k3 = 0; k3 < R3; ++k3)
-                            z[k3] = cmul(z[k3], __ldg(a.ghat + gofs + pfix + revd<RADIX, R3>(k3)));
-                        Dft<R3, -1>::run(z);
+                            for (int k3 = 0; k3 < R3; ++k3) z[k3] = cmul(z[k3], __ldg(gh + revd<RADIX, R3>(k3)));
+                        }
+                        dft<R3, -1>(z);
                         if (k2 != 0) {
+                            const V* tw2 = a.tw2 + k2 * R3;
 #pragma unroll
-                            for (int m3 = 1; m3 < R3; ++m3) z[m3] = cmulc(z[m3], __ldg(a.tw2 + k2 * R3 + m3));
+                            for (int m3 = 1; m3 < R3; ++m3) z[m3] = cmulc(z[m3], __ldg(tw2 + m3));
                         }
 #pragma unroll
-                        for (int m3 = 0; m3 < R3; ++m3) sm[sidx(k1 * R23 + k2 * R3 + m3, c)] = z[m3];
+                        for (int m3 = 0; m3 < R3; ++m3) sp[m3 * SS] = z[m3];
                     }
                 }
             }
@@ -261,112 +298,109 @@ __global__ void __launch_bounds__(256) pass_kernel(PassArgs<T> a) {
         if constexpr (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ || KIND == KIND_CONV) {
             constexpr int S = (KIND == KIND_DIT_FWD) ? 1 : -1;
             constexpr bool FROM_GLOBAL = KIND != KIND_CONV;
-            auto tw = [&](V x, V w) -> V { return S > 0 ? cmul(x, w) : cmulc(x, w); };
+            auto tw = [](V x, V w) -> V { return S > 0 ? cmul(x, w) : cmulc(x, w); };
             // ---------------------------------------- DIT step A (R3 > 1)
             if constexpr (NSTEP == 3 && FROM_GLOBAL) {
-                constexpr int G = R1 * R2;
-                for (int w = tid; w < G * W; w += NT) {
-                    int g, c;
-                    item(w, G, g, c);
+#pragma unroll
+                for (int j = 0; j < Sh::G3 / GMIN; ++j) {
+                    const int g = gt + j * GMIN;
                     const int k1 = g / R2, k2 = g - (g / R2) * R2;
-                    const bool ok = c < nvalid;
                     const int pfix = revd<RADIX, R1>(k1) * R23 + revd<RADIX, R2>(k2) * R3;
+                    const V* gp = gsrc + (long long)pfix * rs;
                     V z[R3];
 #pragma unroll
-                    for (int k3 = 0; k3 < R3; ++k3)
-                        z[k3] = ok ? src[base + (long long)(pfix + revd<RADIX, R3>(k3)) * rs + c * cs] : V{0, 0};
+                    for (int k3 = 0; k3 < R3; ++k3) z[k3] = ok ? gp[(long long)revd<RADIX, R3>(k3) * rs] : V{0, 0};
                     if (a.ext && ok) {
-                        V t, s;
-                        ext_pair(c, k1 + R1 * k2, R1 * R2, t, s);
+                        V w, st;
+                        ext_pair(k1 + R1 * k2, R1 * R2, w, st);
 #pragma unroll
                         for (int k3 = 0; k3 < R3; ++k3) {
-                            z[k3] = tw(z[k3], t);
-                            t = cmul(t, s);
+                            z[k3] = tw(z[k3], w);
+                            w = cmul(w, st);
                         }
                     }
-                    Dft<R3, S>::run(z);
+                    dft<R3, S>(z);
                     if (k2 != 0) {
+                        const V* tw2 = a.tw2 + k2 * R3;
 #pragma unroll
-                        for (int m3 = 1; m3 < R3; ++m3) z[m3] = tw(z[m3], __ldg(a.tw2 + k2 * R3 + m3));
+                        for (int m3 = 1; m3 < R3; ++m3) z[m3] = tw(z[m3], __ldg(tw2 + m3));
                     }
+                    V* sp = scol + (k1 * R23 + k2 * R3) * SS;
 #pragma unroll
-                    for (int m3 = 0; m3 < R3; ++m3) sm[sidx(k1 * R23 + k2 * R3 + m3, c)] = z[m3];
+                    for (int m3 = 0; m3 < R3; ++m3) sp[m3 * SS] = z[m3];
                 }
             }
             // ---------------------------------------- DIT step B (R2 > 1)
             if constexpr (NSTEP >= 2 && !(KIND == KIND_CONV && NSTEP == 2)) {
                 if constexpr (NSTEP == 3) __syncthreads();
-                constexpr int G = R1 * R3;
-                for (int w = tid; w < G * W; w += NT) {
-                    int g, c;
-                    item(w, G, g, c);
+#pragma unroll
+                for (int j = 0; j < Sh::G2 / GMIN; ++j) {
+                    const int g = gt + j * GMIN;
                     const int k1 = g / R3, m3 = g - (g / R3) * R3;
+                    V* sp = scol + (k1 * R23 + m3) * SS;
                     V z[R2];
                     if constexpr (NSTEP == 2 && FROM_GLOBAL) {
-                        const bool ok = c < nvalid;
-                        const int pfix = revd<RADIX, R1>(k1) * R23;
+                        const V* gp = gsrc + (long long)(revd<RADIX, R1>(k1) * R23) * rs;
 #pragma unroll
-                        for (int k2 = 0; k2 < R2; ++k2)
-                            z[k2] = ok ? src[base + (long long)(pfix + revd<RADIX, R2>(k2)) * rs + c * cs] : V{0, 0};
+                        for (int k2 = 0; k2 < R2; ++k2) z[k2] = ok ? gp[(long long)revd<RADIX, R2>(k2) * rs] : V{0, 0};
                         if (a.ext && ok) {
-                            V t, s;
-                            ext_pair(c, k1, R1, t, s);
+                            V w, st;
+                            ext_pair(k1, R1, w, st);
 #pragma unroll
                             for (int k2 = 0; k2 < R2; ++k2) {
-                                z[k2] = tw(z[k2], t);
-                                t = cmul(t, s);
+                                z[k2] = tw(z[k2], w);
+                                w = cmul(w, st);
                             }
                         }
                     } else {
 #pragma unroll
-                        for (int k2 = 0; k2 < R2; ++k2) z[k2] = sm[sidx(k1 * R23 + k2 * R3 + m3, c)];
+                        for (int k2 = 0; k2 < R2; ++k2) z[k2] = sp[k2 * R3 * SS];
                     }
-                    Dft<R2, S>::run(z);
+                    dft<R2, S>(z);
+                    const V* tw1 = a.tw1 + k1 * R23 + m3;
 #pragma unroll
-                    for (int m2 = 0; m2 < R2; ++m2) {
-                        const int m23 = m2 * R3 + m3;
-                        if (m23 != 0) z[m2] = tw(z[m2], __ldg(a.tw1 + k1 * R23 + m23));
-                    }
+                    for (int m2 = 0; m2 < R2; ++m2)
+                        if (m2 * R3 != 0 || m3 != 0) z[m2] = tw(z[m2], __ldg(tw1 + m2 * R3));
 #pragma unroll
-                    for (int m2 = 0; m2 < R2; ++m2) sm[sidx(k1 * R23 + m2 * R3 + m3, c)] = z[m2];
+                    for (int m2 = 0; m2 < R2; ++m2) sp[m2 * R3 * SS] = z[m2];
                 }
             }
             // ---------------------------------------- DIT step C (always)
             if constexpr (!(KIND == KIND_CONV && NSTEP == 1)) {
                 if constexpr (NSTEP >= 2) __syncthreads();
-                constexpr int G = R23;
-                for (int w = tid; w < G * W; w += NT) {
-                    int g, c;
-                    item(w, G, g, c);
-                    const bool ok = c < nvalid;
+#pragma unroll
+                for (int j = 0; j < Sh::G1 / GMIN; ++j) {
+                    const int g = gt + j * GMIN;  // m23
                     V z[R1];
                     if constexpr (NSTEP == 1) {
-                        // single codelet straight from global (DIT kinds only)
 #pragma unroll
                         for (int k1 = 0; k1 < R1; ++k1)
-                            z[k1] = ok ? src[base + (long long)revd<RADIX, R1>(k1) * rs + c * cs] : V{0, 0};
+                            z[k1] = ok ? gsrc[(long long)revd<RADIX, R1>(k1) * rs] : V{0, 0};
                         if (a.ext && ok) {
-                            V t, s;
-                            ext_pair(c, 0, 1, t, s);
+                            V w, st;
+                            ext_pair(0, 1, w, st);
 #pragma unroll
                             for (int k1 = 0; k1 < R1; ++k1) {
-                                z[k1] = tw(z[k1], t);
-                                t = cmul(t, s);
+                                z[k1] = tw(z[k1], w);
+                                w = cmul(w, st);
                             }
                         }
                     } else {
 #pragma unroll
-                        for (int k1 = 0; k1 < R1; ++k1) z[k1] = sm[sidx(k1 * R23 + g, c)];
+                        for (int k1 = 0; k1 < R1; ++k1) z[k1] = scol[(k1 * R23 + g) * SS];
                     }
-                    Dft<R1, S>::run(z);
+                    dft<R1, S>(z);
                     if (ok) {
+                        V* gp = gdst + (long long)g * rs;
 #pragma unroll
                         for (int m1 = 0; m1 < R1; ++m1) {
-                            const long long e = base + (long long)(m1 * R23 + g) * rs + c * cs;
                             V y = z[m1];
-                            if (a.mul) y = cmul(y, __ldg(a.mul + (e % a.N)));
+                            if (a.mul) {
+                                const long long e = (gp - a.dst) + (long long)(m1 * R23) * rs;
+                                y = cmul(y, __ldg(a.mul + (e % a.N)));
+                            }
                             if (a.has_scale) y = V{y.x * a.scale, y.y * a.scale};
-                            dst[e] = y;
+                            gp[(long long)(m1 * R23) * rs] = y;
                         }
                     }
                 }

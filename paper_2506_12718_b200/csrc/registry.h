@@ -12,6 +12,8 @@ struct KernelEntry {
     int radix;
     int R, R1, R2, R3;
     int kind;   // PassKind
+    int map;    // PassMap
+    int W, NT, smem;  // compile-time tile policy of this instance
     const void* fn;
 };
 
@@ -39,5 +41,5 @@ void register_r8_f32(Registry&);
     X(4, 4, 1, 1) X(4, 16, 1, 1) X(4, 16, 4, 1) X(4, 16, 16, 1) X(4, 16, 16, 4) X(4, 16, 16, 16)
 #define PAFFT_SHAPES_R8(X) X(8, 8, 1, 1) X(8, 8, 8, 1) X(8, 8, 8, 8)
 #define PAFFT_SHAPES_R3(X) \
-    X(3, 3, 1, 1) X(3, 9, 1, 1) X(3, 27, 1, 1) X(3, 27, 3, 1) X(3, 27, 9, 1) X(3, 27, 27, 1) X(3, 27, 27, 3)
+    X(3, 3, 1, 1) X(3, 9, 1, 1) X(3, 27, 1, 1) X(3, 27, 3, 1) X(3, 27, 9, 1) X(3, 27, 27, 1) X(3, 27, 9, 9)
 #define PAFFT_SHAPES_R5(X) X(5, 5, 1, 1) X(5, 25, 1, 1) X(5, 25, 5, 1) X(5, 25, 25, 1) X(5, 25, 25, 5)
