@@ -6,6 +6,8 @@
 // (convolution.cpp:45-52), convolve_standard (:37-43) and the transforms
 // (transform.cpp:8-26).  No CPU compute fallback exists: every transform runs
 // in the sm_100a kernels; the host only builds tables and moves buffers.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -122,6 +124,8 @@ struct PassDesc {
     long long K0 = 0, L = 0, sq = 1, C = 1;
     int contig = 0, W = 1, NT = 32;
     size_t smem = 0;
+    long long max_ctas = 1;
+    int use_tmap = 0, rb = 0, sw = 0;  // STRIDED tensor-map staging
     int ext = 0;
     unsigned ext_bits = 0;
     const void* ext_lo = nullptr;
@@ -159,6 +163,7 @@ struct pafft_plan_s {
     std::mutex mu;
     // pass schedules, built once at plan creation (immutable afterwards)
     std::vector<PassDesc> pf, dif, dit_fwd, dit_conj;
+    std::map<std::string, CUtensorMap> tmaps;
 };
 
 struct pafft_filter_s {
@@ -323,9 +328,73 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     const int nstep = 1 + (d.R2 > 1) + (d.R3 > 1);
     if (d.smem > 48 * 1024)
         CUDA_TRY(cudaFuncSetAttribute(d.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
+    {
+        // persistent grid: every resident CTA slot on the device, no more
+        int occ = 0, sms = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, d.fn, d.NT, d.smem));
+        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+        if (occ < 1) return fail(PAFFT_CUDA_ERROR, "pass kernel R=%d cannot be resident (smem %zu)", d.R, d.smem);
+        d.max_ctas = (long long)occ * sms;
+    }
+    if (!d.contig) {
+        // 2-D tensor map staging needs 16-byte row strides (always for fp64,
+        // even C for fp32); otherwise one bulk copy per row.
+        d.sw = p->esize == 8 ? d.W + 2 : d.W;
+        d.use_tmap = (p->esize == 16 || (d.C % 2) == 0) && env_int("PAFFT_NO_TMAP", 0) == 0;
+        int rb = 1;
+        for (int v = 1; v <= 256 && v <= d.R; ++v)
+            if (d.R % v == 0) rb = v;
+        d.rb = rb;
+    }
     d.ext = d.L > 1;
     if (d.ext) ST_TRY(ext_table(p, d.K0, d));
     if (nstep > 1) ST_TRY(int_table(p, d));
+    return PAFFT_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+    });
+    return fn;
+}
+
+// 2-D view of a pass input: rows of C complex (2C reals), box = rb rows x sw
+// complex columns.  Cached per (buffer, geometry).
+pafft_status tensor_map(pafft_plan_t p, const PassDesc& d, const void* src, size_t batch, CUtensorMap* out) {
+    const unsigned long long rows = (unsigned long long)p->total * batch / (unsigned long long)d.C;
+    char key[160];
+    snprintf(key, sizeof key, "%p/%lld/%llu/%d/%d/%d", src, d.C, rows, d.sw, d.rb, p->prec);
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        auto it = p->tmaps.find(key);
+        if (it != p->tmaps.end()) {
+            *out = it->second;
+            return PAFFT_OK;
+        }
+    }
+    auto enc = encode_fn();
+    if (!enc) return fail(PAFFT_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)(2 * d.C), (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(d.C * p->esize)};
+    const cuuint32_t box[2] = {(cuuint32_t)(2 * d.sw), (cuuint32_t)d.rb};
+    const cuuint32_t estr[2] = {1, 1};
+    CUtensorMap m;
+    const CUresult r = enc(&m, p->prec == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                           const_cast<void*>(src), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PAFFT_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    std::lock_guard<std::mutex> lk(p->mu);
+    if (p->tmaps.size() > 4096) p->tmaps.clear();
+    p->tmaps[key] = m;
+    *out = m;
     return PAFFT_OK;
 }
 
@@ -355,8 +424,13 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     a.scale = (T)scale;
     a.has_scale = scale != 1.0;
     if (a.tiles == 0) return PAFFT_OK;
-    const long long grid = std::min<long long>(a.tiles, 0x7fffffffll);
-    void* args[] = {&a};
+    CUtensorMap map;
+    memset(&map, 0, sizeof map);
+    a.use_tmap = d.use_tmap;
+    a.rb = d.rb;
+    if (d.use_tmap) ST_TRY(tensor_map(p, d, src, batch, &map));
+    const long long grid = std::min<long long>(a.tiles, d.max_ctas);
+    void* args[] = {&a, &map};
     CUDA_TRY(cudaLaunchKernel(d.fn, dim3((unsigned)grid), dim3(d.NT), args, d.smem, st));
     ++g_launches;
     return PAFFT_OK;

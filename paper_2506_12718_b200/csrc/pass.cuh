@@ -32,6 +32,8 @@
 // immediates.  Layout is interleaved complex (double2 / float2).
 #pragma once
 
+#include <cuda.h>
+
 #include "codelets.cuh"
 
 namespace pafft_b200 {
@@ -63,6 +65,10 @@ template <typename T> struct PassArgs {
     const cplx<T>* mul;
     T scale;
     int has_scale;
+    // STRIDED staging through a 2-D tensor map (boxes of rb rows), else one
+    // bulk copy per row
+    int use_tmap;
+    int rb;
 };
 
 // Base-r digit reversal over the digits of P = r^s (permutation.cpp:27-37).
@@ -95,22 +101,36 @@ template <int R1, int R2, int R3> struct Shape {
 template <typename T, int R1, int R2, int R3, int MAP> struct TilePolicy {
     using S = Shape<R1, R2, R3>;
     static constexpr int ESZ = (int)sizeof(cplx<T>);
-    static constexpr int SMEM_BUDGET = 112 * 1024;
+    static constexpr int SMEM_BUDGET = 110 * 1024;  // per tile buffer (two are resident)
     // STRIDED: 8 (fp64) / 16 (fp32) columns = one 128-byte row segment; more
     // columns for single-codelet passes (no shared memory, tiny groups).
     static constexpr int MAXW = MAP == MAP_STRIDED ? (S::NSTEP == 1 ? 64 : (ESZ == 16 ? 8 : 16)) : 64;
+    // fp32 strided rows may start 8 bytes off a 16-byte boundary (odd C):
+    // each shared row then holds W + 2 slots and the data sits at a per-row
+    // shift of 0 or 1 element (see stage_tile).
+    static constexpr bool SHIFT = MAP == MAP_STRIDED && ESZ == 8;
+    static constexpr int rowslots(int w) { return SHIFT ? w + 2 : w; }
     static constexpr int wcalc() {
         int w = MAXW;
         while (w > 1 && S::GMIN * w > 512) --w;
         if (MAP == MAP_CONTIG)
             while (w > 1 && S::GMIN * w > 256) --w;
-        if (S::NSTEP > 1)
-            while (w > 1 && S::R * w * ESZ > SMEM_BUDGET) --w;
+        while (w > 1 && S::R * rowslots(w) * ESZ > SMEM_BUDGET) --w;
+        // at least one full warp: warp 0 issues the bulk copies
+        while (S::GMIN * w < 32 && S::R * rowslots(w + 1) * ESZ <= SMEM_BUDGET) ++w;
+        if (SHIFT && (w & 1)) ++w;  // even W keeps rows 16-byte sized
+        // fp32 contiguous tiles start at first*R elements: even W keeps every
+        // tile start 16-byte aligned for the bulk copy
+        if (MAP == MAP_CONTIG && ESZ == 8 && (w & 1)) w = (w > 1 && S::R * (w + 1) * ESZ > SMEM_BUDGET) ? w - 1 : w + 1;
         return w;
     }
     static constexpr int W = wcalc();
+    static constexpr int SW = rowslots(W);  // shared row stride (STRIDED)
     static constexpr int NT = S::GMIN * W;
-    static constexpr int SMEM = S::NSTEP > 1 ? S::R * W * ESZ : 0;
+    static_assert(NT >= 32, "tile policy needs a full warp");
+    // two tile buffers (TMA double buffering) + two mbarriers
+    static constexpr int BUF = ((MAP == MAP_STRIDED ? S::R * SW : S::R * W) * ESZ + 15) / 16 * 16;
+    static constexpr int SMEM = 2 * BUF + 16;
 };
 
 template <typename T>
@@ -120,52 +140,194 @@ __device__ __forceinline__ cplx<T> ext_root(const PassArgs<T>& a, unsigned long 
     return cmul(lo, hi);
 }
 
+// ---------------------------------------------------------------- TMA/mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    unsigned ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!ok);
+}
+// 1-D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Tile geometry: element (row j, tile column c) lives at
+// src + base + j*rs + c*cs; STRIDED: cs = 1, rs = C; CONTIG: cs = R, rs = 1.
+struct TileGeo {
+    long long base;   // element offset of (row 0, column 0)
+    long long first;  // first column (STRIDED) or first panel (CONTIG)
+    int nvalid;
+};
+
+template <int R, int W, bool STRIDED, typename T>
+__device__ __forceinline__ TileGeo tile_geo(const PassArgs<T>& a, long long tile) {
+    TileGeo g;
+    if (!STRIDED) {
+        g.first = tile * W;
+        const long long left = a.panels - g.first;
+        g.nvalid = left < W ? (int)left : W;
+        g.base = g.first * (long long)R;
+    } else {
+        const long long p = tile / a.tiles_per_panel;
+        g.first = (tile - p * a.tiles_per_panel) * (long long)W;
+        const long long left = a.C - g.first;
+        g.nvalid = left < W ? (int)left : W;
+        g.base = p * a.panel_elems + g.first;
+    }
+    return g;
+}
+
+// Issue the bulk copies that stage one tile into `buf` (called by warp 0).
+// STRIDED: one copy per row (rows land at buf[j*SW + shift_j]); CONTIG: the
+// tile is one contiguous run of nvalid*R elements.  Bulk copies need 16-byte
+// aligned addresses and sizes: fp64 always satisfies this; fp32 rows copy the
+// enclosing 16-byte-aligned window (shift_j = 1 when the row starts 8 bytes
+// into it), and an odd fp32 contiguous tail element is moved by one thread.
+__device__ __forceinline__ void tma_load_2d(void* sdst, const CUtensorMap* map, int x, int y,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(sdst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int R, int W, int SW, bool STRIDED, typename T>
+__device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorMap* map, long long tile,
+                                           cplx<T>* buf, unsigned long long* bar, int lane) {
+    using V = cplx<T>;
+    const TileGeo g = tile_geo<R, W, STRIDED>(a, tile);
+    if (STRIDED && a.use_tmap) {
+        // boxes of rb rows x SW columns (out-of-range columns zero-filled);
+        // the tile lands densely as [row][SW]
+        if (lane == 0) {
+            const long long p = tile / a.tiles_per_panel;
+            const int nb = R / a.rb;
+            mbar_expect_tx(bar, (unsigned)(R * SW * sizeof(V)));
+            for (int i = 0; i < nb; ++i)
+                tma_load_2d(buf + i * a.rb * SW, map, (int)(2 * g.first), (int)(p * R + i * a.rb), bar);
+        }
+    } else if (STRIDED) {
+        const V* src = a.src + g.base;
+        if constexpr (sizeof(V) == 16) {
+            const unsigned rb = (unsigned)(g.nvalid * sizeof(V));
+            if (lane == 0) mbar_expect_tx(bar, rb * R);
+            __syncwarp();
+            for (int j = lane; j < R; j += 32) tma_load_1d(buf + j * SW, src + (long long)j * a.C, rb, bar);
+        } else {
+            // total bytes: sum over rows of round16(shift_j*8 + nvalid*8)
+            const long long b0 = g.base & 1;
+            const unsigned odd = (unsigned)(a.C & 1);
+            const unsigned n8 = (unsigned)g.nvalid * 8u;
+            const unsigned sz0 = (n8 + 15u) & ~15u;              // shift 0
+            const unsigned sz1 = (n8 + 8u + 15u) & ~15u;         // shift 1
+            const unsigned rows_shift1 = odd ? (unsigned)(b0 ? (R + 1) / 2 : R / 2) : (unsigned)(b0 ? R : 0);
+            if (lane == 0) mbar_expect_tx(bar, rows_shift1 * sz1 + ((unsigned)R - rows_shift1) * sz0);
+            __syncwarp();
+            for (int j = lane; j < R; j += 32) {
+                const unsigned sh = (unsigned)(b0 ^ (j & odd));
+                const V* row = src + (long long)j * a.C - sh;
+                tma_load_1d(buf + j * SW, row, sh ? sz1 : sz0, bar);
+            }
+        }
+    } else if (lane == 0) {
+        const long long n = (long long)g.nvalid * R;
+        unsigned bytes = (unsigned)(n * sizeof(V));
+        if constexpr (sizeof(V) == 8) {
+            if (bytes & 15u) {  // odd element count: tail element by hand
+                bytes -= 8u;
+                buf[n - 1] = a.src[g.base + n - 1];
+            }
+        }
+        mbar_expect_tx(bar, bytes);
+        if (bytes) tma_load_1d(buf, a.src + g.base, bytes, bar);
+    }
+}
+
+// Persistent pass kernel: each CTA walks tiles blockIdx.x + i * gridDim.x.
+// Tile i+1 streams into the other shared buffer (TMA, mbarrier) while tile i
+// is transformed in place in its buffer; results go straight from registers
+// to global memory in their final order (rev-ordered rows for DIF).
 template <typename T, int RADIX, int R1, int R2, int R3, int KIND, int MAP>
-__global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
-    pass_kernel(const PassArgs<T> a) {
+__global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT, 1)
+    pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap) {
     using V = cplx<T>;
     using Sh = Shape<R1, R2, R3>;
     using Pol = TilePolicy<T, R1, R2, R3, MAP>;
     constexpr int R = Sh::R, R23 = Sh::R23, NSTEP = Sh::NSTEP, GMIN = Sh::GMIN;
     constexpr int W = Pol::W;
+    constexpr int SW = Pol::SW;
+    constexpr int BUFE = Pol::BUF / (int)sizeof(V);  // elements per tile buffer
     constexpr bool STRIDED = MAP == MAP_STRIDED;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    V* const sm = reinterpret_cast<V*>(smem_raw);
+    constexpr bool SHIFT = Pol::SHIFT;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    V* const bufs = reinterpret_cast<V*>(smem_raw);
+    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem_raw + 2 * Pol::BUF);
 
     const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
     // thread -> (tile column c, group slot gt); STRIDED: c fastest (coalesced
     // W-wide row segments, conflict-free smem rows); CONTIG: group fastest.
     const int c = STRIDED ? t % W : t / GMIN;
     const int gt = STRIDED ? t / W : t % GMIN;
-    // shared element (j, c): STRIDED sm[j*W + c], CONTIG sm[c*R + j]
-    V* const scol = STRIDED ? sm + c : sm + c * R;
-    constexpr int SS = STRIDED ? W : 1;  // shared stride between consecutive j
+    constexpr int SS = STRIDED ? SW : 1;  // shared stride between consecutive rows
+    const long long rs = STRIDED ? (long long)a.C : 1;  // global row stride
 
-    for (long long tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
-        long long base, first;
-        int nvalid;
-        if (!STRIDED) {
-            first = tile * W;
-            const long long left = a.panels - first;
-            nvalid = left < W ? (int)left : W;
-            base = first * (long long)R + (long long)c * R;
-        } else {
-            const long long p = tile / a.tiles_per_panel;
-            first = (tile - p * a.tiles_per_panel) * (long long)W;
-            const long long left = a.C - first;
-            nvalid = left < W ? (int)left : W;
-            base = p * a.panel_elems + first + c;
-        }
-        const bool ok = c < nvalid;
-        const long long rs = STRIDED ? (long long)a.C : 1;  // global row stride
-        const V* __restrict__ gsrc = a.src + base;
-        V* __restrict__ gdst = a.dst + base;
-        // external twiddle base/step for this column: w_K0^{jj kf}, w_K0^{jj S}
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long t0 = blockIdx.x, ts = gridDim.x;
+    if (warp == 0) {
+        if (t0 < a.tiles) stage_tile<R, W, SW, STRIDED>(a, &tmap, t0, bufs, &bars[0], lane);
+        if (t0 + ts < a.tiles) stage_tile<R, W, SW, STRIDED>(a, &tmap, t0 + ts, bufs + BUFE, &bars[1], lane);
+    }
+    __syncthreads();  // hand-copied fp32 tail elements of the first tiles
+
+    int it = 0;
+    for (long long tile = t0; tile < a.tiles; tile += ts, ++it) {
+        const int b = it & 1;
+        V* const buf = bufs + b * BUFE;
+        const TileGeo geo = tile_geo<R, W, STRIDED>(a, tile);
+        const long long first = geo.first;
+        const bool ok = c < geo.nvalid;
+        V* const scol = STRIDED ? buf + c : buf + c * R;
+        // shared element of tile row `row` for this thread's column
+        const int codd = SHIFT && !a.use_tmap ? (a.C & 1) : 0;
+        const int b0 = SHIFT && !a.use_tmap ? (int)(geo.base & 1) : 0;
+        auto sref = [&](int row) -> V& { return scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)]; };
+        V* __restrict__ gdst = a.dst + geo.base + (STRIDED ? c : (long long)c * R);
         auto ext_pair = [&](int kf, int S, V& tw, V& st) {
             const unsigned long long jj = (unsigned long long)(first + c) / a.sq;
             tw = ext_root(a, jj * (unsigned long long)kf);
             st = ext_root(a, jj * (unsigned long long)S);
         };
+        mbar_wait(&bars[b], (it >> 1) & 1);
 
         if constexpr (KIND == KIND_DIF || KIND == KIND_CONV) {
             // ------------------------------------------------ DIF step 1
@@ -174,8 +336,7 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                 const int g = gt + j * GMIN;  // m23
                 V z[R1];
 #pragma unroll
-                for (int m1 = 0; m1 < R1; ++m1)
-                    z[m1] = ok ? gsrc[(long long)(m1 * R23 + g) * rs] : V{0, 0};
+                for (int m1 = 0; m1 < R1; ++m1) z[m1] = sref(m1 * R23 + g);
                 dft<R1, 1>(z);
                 if constexpr (NSTEP == 1) {
                     if constexpr (KIND == KIND_DIF) {
@@ -203,7 +364,7 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
 #pragma unroll
                     for (int k1 = 1; k1 < R1; ++k1) z[k1] = cmul(z[k1], __ldg(tw1 + k1 * R23));
 #pragma unroll
-                    for (int k1 = 0; k1 < R1; ++k1) scol[(k1 * R23 + g) * SS] = z[k1];
+                    for (int k1 = 0; k1 < R1; ++k1) sref(k1 * R23 + g) = z[k1];
                 }
             }
             if constexpr (NSTEP >= 2) {
@@ -213,10 +374,10 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                 for (int j = 0; j < Sh::G2 / GMIN; ++j) {
                     const int g = gt + j * GMIN;
                     const int k1 = g / R3, m3 = g - (g / R3) * R3;
-                    V* sp = scol + (k1 * R23 + m3) * SS;
+                    const int sb = k1 * R23 + m3;
                     V z[R2];
 #pragma unroll
-                    for (int m2 = 0; m2 < R2; ++m2) z[m2] = sp[m2 * R3 * SS];
+                    for (int m2 = 0; m2 < R2; ++m2) z[m2] = sref(sb + m2 * R3);
                     dft<R2, 1>(z);
                     if constexpr (NSTEP == 2) {
                         const int pfix = revd<RADIX, R1>(k1) * R23;
@@ -224,9 +385,10 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                             if (ok) {
                                 V tw{1, 0}, st{1, 0};
                                 if (a.ext) ext_pair(k1, R1, tw, st);
+                                V* gp = gdst + (long long)pfix * rs;
 #pragma unroll
                                 for (int k2 = 0; k2 < R2; ++k2) {
-                                    gdst[(long long)(pfix + revd<RADIX, R2>(k2)) * rs] = a.ext ? cmul(z[k2], tw) : z[k2];
+                                    gp[(long long)revd<RADIX, R2>(k2) * rs] = a.ext ? cmul(z[k2], tw) : z[k2];
                                     if (a.ext) tw = cmul(tw, st);
                                 }
                             }
@@ -241,14 +403,14 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
 #pragma unroll
                             for (int m2 = 1; m2 < R2; ++m2) z[m2] = cmulc(z[m2], __ldg(tw1 + m2));
 #pragma unroll
-                            for (int m2 = 0; m2 < R2; ++m2) sp[m2 * SS] = z[m2];
+                            for (int m2 = 0; m2 < R2; ++m2) sref(sb + m2) = z[m2];
                         }
                     } else {
                         const V* tw2 = a.tw2 + m3;
 #pragma unroll
                         for (int k2 = 1; k2 < R2; ++k2) z[k2] = cmul(z[k2], __ldg(tw2 + k2 * R3));
 #pragma unroll
-                        for (int k2 = 0; k2 < R2; ++k2) sp[k2 * R3 * SS] = z[k2];
+                        for (int k2 = 0; k2 < R2; ++k2) sref(sb + k2 * R3) = z[k2];
                     }
                 }
             }
@@ -259,10 +421,10 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                 for (int j = 0; j < Sh::G3 / GMIN; ++j) {
                     const int g = gt + j * GMIN;
                     const int k1 = g / R2, k2 = g - (g / R2) * R2;
-                    V* sp = scol + (k1 * R23 + k2 * R3) * SS;
+                    const int sb = k1 * R23 + k2 * R3;
                     V z[R3];
 #pragma unroll
-                    for (int m3 = 0; m3 < R3; ++m3) z[m3] = sp[m3 * SS];
+                    for (int m3 = 0; m3 < R3; ++m3) z[m3] = sref(sb + m3);
                     dft<R3, 1>(z);
                     const int pfix = revd<RADIX, R1>(k1) * R23 + revd<RADIX, R2>(k2) * R3;
                     if constexpr (KIND == KIND_DIF) {
@@ -289,7 +451,7 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                             for (int m3 = 1; m3 < R3; ++m3) z[m3] = cmulc(z[m3], __ldg(tw2 + m3));
                         }
 #pragma unroll
-                        for (int m3 = 0; m3 < R3; ++m3) sp[m3 * SS] = z[m3];
+                        for (int m3 = 0; m3 < R3; ++m3) sref(sb + m3) = z[m3];
                     }
                 }
             }
@@ -297,19 +459,18 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
 
         if constexpr (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ || KIND == KIND_CONV) {
             constexpr int S = (KIND == KIND_DIT_FWD) ? 1 : -1;
-            constexpr bool FROM_GLOBAL = KIND != KIND_CONV;
+            constexpr bool FIRST = KIND != KIND_CONV;  // DIT kinds start from the staged input
             auto tw = [](V x, V w) -> V { return S > 0 ? cmul(x, w) : cmulc(x, w); };
             // ---------------------------------------- DIT step A (R3 > 1)
-            if constexpr (NSTEP == 3 && FROM_GLOBAL) {
+            if constexpr (NSTEP == 3 && FIRST) {
 #pragma unroll
                 for (int j = 0; j < Sh::G3 / GMIN; ++j) {
                     const int g = gt + j * GMIN;
                     const int k1 = g / R2, k2 = g - (g / R2) * R2;
                     const int pfix = revd<RADIX, R1>(k1) * R23 + revd<RADIX, R2>(k2) * R3;
-                    const V* gp = gsrc + (long long)pfix * rs;
                     V z[R3];
 #pragma unroll
-                    for (int k3 = 0; k3 < R3; ++k3) z[k3] = ok ? gp[(long long)revd<RADIX, R3>(k3) * rs] : V{0, 0};
+                    for (int k3 = 0; k3 < R3; ++k3) z[k3] = sref(pfix + revd<RADIX, R3>(k3));
                     if (a.ext && ok) {
                         V w, st;
                         ext_pair(k1 + R1 * k2, R1 * R2, w, st);
@@ -325,24 +486,28 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
 #pragma unroll
                         for (int m3 = 1; m3 < R3; ++m3) z[m3] = tw(z[m3], __ldg(tw2 + m3));
                     }
-                    V* sp = scol + (k1 * R23 + k2 * R3) * SS;
+                    // in place: the rows pfix + rev(k3) just read are rows pfix + m3
 #pragma unroll
-                    for (int m3 = 0; m3 < R3; ++m3) sp[m3 * SS] = z[m3];
+                    for (int m3 = 0; m3 < R3; ++m3) sref(pfix + m3) = z[m3];
                 }
             }
             // ---------------------------------------- DIT step B (R2 > 1)
+            // Slot convention: DIT kinds keep the staged (digit-reversed) row
+            // order, so group k1 lives at rev(k1)*R23 and index k2 at rev(k2)*R3;
+            // CONV continues from the DIF's natural frequency slots.  Every step
+            // then reads and writes the same slot set (in place).
             if constexpr (NSTEP >= 2 && !(KIND == KIND_CONV && NSTEP == 2)) {
                 if constexpr (NSTEP == 3) __syncthreads();
 #pragma unroll
                 for (int j = 0; j < Sh::G2 / GMIN; ++j) {
                     const int g = gt + j * GMIN;
                     const int k1 = g / R3, m3 = g - (g / R3) * R3;
-                    V* sp = scol + (k1 * R23 + m3) * SS;
+                    const int sk1 = FIRST ? revd<RADIX, R1>(k1) : k1;
+                    const int sb = sk1 * R23 + m3;
                     V z[R2];
-                    if constexpr (NSTEP == 2 && FROM_GLOBAL) {
-                        const V* gp = gsrc + (long long)(revd<RADIX, R1>(k1) * R23) * rs;
 #pragma unroll
-                        for (int k2 = 0; k2 < R2; ++k2) z[k2] = ok ? gp[(long long)revd<RADIX, R2>(k2) * rs] : V{0, 0};
+                    for (int k2 = 0; k2 < R2; ++k2) z[k2] = sref(sb + (FIRST ? revd<RADIX, R2>(k2) : k2) * R3);
+                    if constexpr (NSTEP == 2 && FIRST) {
                         if (a.ext && ok) {
                             V w, st;
                             ext_pair(k1, R1, w, st);
@@ -352,9 +517,6 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                                 w = cmul(w, st);
                             }
                         }
-                    } else {
-#pragma unroll
-                        for (int k2 = 0; k2 < R2; ++k2) z[k2] = sp[k2 * R3 * SS];
                     }
                     dft<R2, S>(z);
                     const V* tw1 = a.tw1 + k1 * R23 + m3;
@@ -362,7 +524,7 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                     for (int m2 = 0; m2 < R2; ++m2)
                         if (m2 * R3 != 0 || m3 != 0) z[m2] = tw(z[m2], __ldg(tw1 + m2 * R3));
 #pragma unroll
-                    for (int m2 = 0; m2 < R2; ++m2) sp[m2 * R3 * SS] = z[m2];
+                    for (int m2 = 0; m2 < R2; ++m2) sref(sb + m2 * R3) = z[m2];
                 }
             }
             // ---------------------------------------- DIT step C (always)
@@ -374,8 +536,7 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                     V z[R1];
                     if constexpr (NSTEP == 1) {
 #pragma unroll
-                        for (int k1 = 0; k1 < R1; ++k1)
-                            z[k1] = ok ? gsrc[(long long)revd<RADIX, R1>(k1) * rs] : V{0, 0};
+                        for (int k1 = 0; k1 < R1; ++k1) z[k1] = sref(revd<RADIX, R1>(k1));
                         if (a.ext && ok) {
                             V w, st;
                             ext_pair(0, 1, w, st);
@@ -387,7 +548,8 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                         }
                     } else {
 #pragma unroll
-                        for (int k1 = 0; k1 < R1; ++k1) z[k1] = scol[(k1 * R23 + g) * SS];
+                        for (int k1 = 0; k1 < R1; ++k1)
+                            z[k1] = sref((FIRST ? revd<RADIX, R1>(k1) : k1) * R23 + g);
                     }
                     dft<R1, S>(z);
                     if (ok) {
@@ -406,7 +568,12 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT)
                 }
             }
         }
+        // all reads of this buffer are done: refill it with tile it + 2
         __syncthreads();
+        if (warp == 0 && tile + 2 * ts < a.tiles) {
+            fence_proxy_async();
+            stage_tile<R, W, SW, STRIDED>(a, &tmap, tile + 2 * ts, buf, &bars[b], lane);
+        }
     }
 }
 
