@@ -267,20 +267,20 @@ def main():
     calls = cfg.calls if cfg.calls > 1 else 1
     bpc = per // calls  # signals per call
     sptr = C.c_void_p(stream.cuda_stream)
+    chunk = int(pf.lib.pafft_plan_chunk_signals(plan._h)) or bpc
+    chunk = max(1, min(chunk, bpc))
+    esz = x.element_size()
 
     def launch_pass(i, xs, ys, nb):
         pf._check(pf.lib.pafft_convolve_permfree_pass(plan._h, filt._h, C.c_void_p(xs), C.c_void_p(ys), nb, i, sptr))
 
-    def step(events=None):
+    def step():
+        # the public hot-path call: convolve_permfree out of place, per call
         for c in range(calls):
-            xs = x.data_ptr() + c * bpc * N * x.element_size()
-            ys = y.data_ptr() + c * bpc * N * y.element_size()
-            for i in range(npass):
-                if events is not None:
-                    events[i][0].record(stream)
-                launch_pass(i, xs, ys, bpc)
-                if events is not None:
-                    events[i][1].record(stream)
+            xs = x.data_ptr() + c * bpc * N * esz
+            ys = y.data_ptr() + c * bpc * N * esz
+            pf._check(pf.lib.pafft_convolve_permfree_oop(plan._h, filt._h, C.c_void_p(xs), C.c_void_p(ys), bpc,
+                                                         sptr))
 
     gpu_index = local
     cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -299,9 +299,6 @@ def main():
         dist.barrier()
 
     # ---- timed region (device-resident, CUDA events, max over ranks)
-    use_pass_events = calls == 1
-    pev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(npass)]
-           for _ in range(args.steps)]
     launches0 = pf.kernel_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -310,7 +307,7 @@ def main():
     tw0 = time.time()
     e0.record(stream)
     for k in range(args.steps):
-        step(pev[k] if use_pass_events else None)
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
     tw1 = time.time()
@@ -331,20 +328,25 @@ def main():
     sampler.stop()
     clocks = sampler.summary(tw0 - 0.05, tw_end + 0.05)
 
-    # per-pass device time (timed steps; for config 1 a separate evented loop)
-    if not use_pass_events:
-        pev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(npass)]
-               for _ in range(max(1, args.steps // 2))]
-        for k in range(len(pev)):
-            xs, ys = x.data_ptr(), y.data_ptr()
+    # ---- per-pass device time: the same launches the pipeline issues (one
+    # L2 chunk per launch), run one at a time on one stream between CUDA events
+    reps = max(1, min(args.steps, 8))
+    nch = max(1, bpc // chunk)
+    pev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(npass)]
+           for _ in range(reps * nch)]
+    for r in range(reps):
+        for q in range(nch):
+            xs = x.data_ptr() + q * chunk * N * esz
+            ys = y.data_ptr() + q * chunk * N * esz
             for i in range(npass):
-                pev[k][i][0].record(stream)
-                launch_pass(i, xs, ys, bpc)
-                pev[k][i][1].record(stream)
-        torch.cuda.synchronize()
+                ev = pev[r * nch + q][i]
+                ev[0].record(stream)
+                launch_pass(i, xs, ys, chunk)
+                ev[1].record(stream)
+    torch.cuda.synchronize()
     pass_ms = [statistics.mean(ev[i][0].elapsed_time(ev[i][1]) for ev in pev) for i in range(npass)]
     dom = max(range(npass), key=lambda i: pass_ms[i])
-    dom_bytes = 2.0 * S * bpc + (S if infos[dom]["kind"] == "conv_mid" else 0.0)
+    dom_bytes = 2.0 * S * chunk + (S if infos[dom]["kind"] == "conv_mid" else 0.0)
     peak, peak_src = measured_peak()
     achieved = dom_bytes / (pass_ms[dom] * 1e-3) / 1e9
 
@@ -419,6 +421,7 @@ def main():
                          "frac": achieved / peak, "traffic": ncu_traffic(f"config{cfg.idx}_{cfg.precision}"),
                          "kernel": f"pass{dom}:{infos[dom]['kind']}(R={infos[dom]['R']})",
                          "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": pass_ms[dom],
+                         "signals_per_launch": chunk,
                          "peak_source": peak_src},
             "conv_roofline": {"bytes_per_conv": workload.bytes_per_conv(cfg, world), "achieved_gbs_per_gpu": conv_gbs,
                               "frac_of_hbm": conv_gbs / peak, "flops_per_conv": flops,

@@ -120,7 +120,7 @@ struct DevBuf {
 struct PassDesc {
     int kind = 0;
     int axis = 0, a = 0, s = 0;
-    int R = 0, R1 = 1, R2 = 1, R3 = 1;
+    int R = 0, F[4] = {1, 1, 1, 1}, nsteps = 1;
     long long K0 = 0, L = 0, sq = 1, C = 1;
     int contig = 0, W = 1, NT = 32;
     size_t smem = 0;
@@ -130,8 +130,7 @@ struct PassDesc {
     unsigned ext_bits = 0;
     const void* ext_lo = nullptr;
     const void* ext_hi = nullptr;
-    const void* tw1 = nullptr;
-    const void* tw2 = nullptr;
+    const void* tw[3] = {nullptr, nullptr, nullptr};
     const void* fn = nullptr;
 };
 
@@ -153,13 +152,15 @@ struct pafft_plan_s {
     std::vector<Group> groups;                 // DIF order; last = contiguous axis-0 group
     std::vector<std::unique_ptr<DevBuf>> owned;
     std::map<long long, std::pair<const void*, const void*>> ext_tables;  // K0 -> (lo, hi)
-    std::map<int, std::pair<const void*, const void*>> int_tables;        // R -> (tw1, tw2)
+    std::map<std::string, std::vector<const void*>> int_tables;            // split -> step tables
     std::map<long long, unsigned> ext_bits;
     std::vector<uint32_t*> rev_dev;            // per-axis digit reversal maps (device)
     // scratch for permutation / host pipelines
     std::unique_ptr<DevBuf> scratch;
     std::unique_ptr<DevBuf> stage[3];
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t work[2] = {nullptr, nullptr};  // L2-chunk pipeline streams
+    cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
     std::mutex mu;
     // pass schedules, built once at plan creation (immutable afterwards)
     std::vector<PassDesc> pf, dif, dit_fwd, dit_conj;
@@ -228,24 +229,29 @@ pafft_status ext_table(pafft_plan_t p, long long K0, PassDesc& d) {
     return PAFFT_OK;
 }
 
+// Internal twiddles of step i: tw[i][k * Q_i + lo] = w_{P_i}^{k lo}
+// (P_i = F_i ... F_last, Q_i = P_i / F_i), keyed by the split.
 pafft_status int_table(pafft_plan_t p, PassDesc& d) {
-    auto it = p->int_tables.find(d.R);
+    char key[64];
+    snprintf(key, sizeof key, "%d/%d/%d/%d", d.F[0], d.F[1], d.F[2], d.F[3]);
+    auto it = p->int_tables.find(key);
     if (it == p->int_tables.end()) {
-        const int R = d.R, R1 = d.R1, R23 = d.R2 * d.R3, R3 = d.R3;
-        std::vector<long double> r1(R), i1(R), r2(R23), i2(R23);
-        for (int k1 = 0; k1 < R1; ++k1)
-            for (int m = 0; m < R23; ++m) root((unsigned long long)k1 * m, R, r1[k1 * R23 + m], i1[k1 * R23 + m]);
-        for (int k2 = 0; k2 < d.R2; ++k2)
-            for (int m3 = 0; m3 < R3; ++m3)
-                root((unsigned long long)k2 * m3, R23, r2[k2 * R3 + m3], i2[k2 * R3 + m3]);
-        const void *t1, *t2;
-        ST_TRY(upload(p, r1, i1, &t1));
-        ST_TRY(upload(p, r2, i2, &t2));
-        p->int_tables[R] = {t1, t2};
-        it = p->int_tables.find(R);
+        std::vector<const void*> tabs;
+        for (int i = 0; i + 1 < d.nsteps; ++i) {
+            long long P = 1;
+            for (int j = i; j < d.nsteps; ++j) P *= d.F[j];
+            const long long Q = P / d.F[i];
+            std::vector<long double> re(P), im(P);
+            for (long long k = 0; k < d.F[i]; ++k)
+                for (long long lo = 0; lo < Q; ++lo) root((unsigned long long)(k * lo), P, re[k * Q + lo], im[k * Q + lo]);
+            const void* t;
+            ST_TRY(upload(p, re, im, &t));
+            tabs.push_back(t);
+        }
+        p->int_tables[key] = tabs;
+        it = p->int_tables.find(key);
     }
-    d.tw1 = it->second.first;
-    d.tw2 = it->second.second;
+    for (size_t i = 0; i < 3; ++i) d.tw[i] = i < it->second.size() ? it->second[i] : nullptr;
     return PAFFT_OK;
 }
 
@@ -319,13 +325,14 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
         return fail(PAFFT_INVALID_ARGUMENT, "no kernel for radix %u R=%d kind %d map %d", p->radix, d.R, kind,
                     d.contig);
     d.fn = ke->fn;
-    d.R1 = ke->R1;
-    d.R2 = ke->R2;
-    d.R3 = ke->R3;
+    d.F[0] = ke->F0;
+    d.F[1] = ke->F1;
+    d.F[2] = ke->F2;
+    d.F[3] = ke->F3;
+    d.nsteps = 1 + (d.F[1] > 1) + (d.F[2] > 1) + (d.F[3] > 1);
     d.W = ke->W;
     d.NT = ke->NT;
     d.smem = (size_t)ke->smem;
-    const int nstep = 1 + (d.R2 > 1) + (d.R3 > 1);
     if (d.smem > 48 * 1024)
         CUDA_TRY(cudaFuncSetAttribute(d.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
     {
@@ -348,7 +355,7 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     }
     d.ext = d.L > 1;
     if (d.ext) ST_TRY(ext_table(p, d.K0, d));
-    if (nstep > 1) ST_TRY(int_table(p, d));
+    if (d.nsteps > 1) ST_TRY(int_table(p, d));
     return PAFFT_OK;
 }
 
@@ -400,7 +407,7 @@ pafft_status tensor_map(pafft_plan_t p, const PassDesc& d, const void* src, size
 
 template <typename T>
 pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
-                      const void* ghat, const void* mul, double scale, cudaStream_t st) {
+                      const void* ghat, const void* mul, double scale, cudaStream_t st, long long grid_cap) {
     PassArgs<T> a;
     memset(&a, 0, sizeof a);
     a.src = (const cplx<T>*)src;
@@ -416,8 +423,7 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     a.ext_bits = d.ext_bits;
     a.ext_lo = (const cplx<T>*)d.ext_lo;
     a.ext_hi = (const cplx<T>*)d.ext_hi;
-    a.tw1 = (const cplx<T>*)d.tw1;
-    a.tw2 = (const cplx<T>*)d.tw2;
+    for (int i = 0; i < 3; ++i) a.tw[i] = (const cplx<T>*)d.tw[i];
     a.ghat = (const cplx<T>*)ghat;
     a.N = (long long)p->total;
     a.mul = (const cplx<T>*)mul;
@@ -429,7 +435,7 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     a.use_tmap = d.use_tmap;
     a.rb = d.rb;
     if (d.use_tmap) ST_TRY(tensor_map(p, d, src, batch, &map));
-    const long long grid = std::min<long long>(a.tiles, d.max_ctas);
+    const long long grid = std::max<long long>(1, std::min<long long>(a.tiles, grid_cap > 0 ? std::min(grid_cap, d.max_ctas) : d.max_ctas));
     void* args[] = {&a, &map};
     CUDA_TRY(cudaLaunchKernel(d.fn, dim3((unsigned)grid), dim3(d.NT), args, d.smem, st));
     ++g_launches;
@@ -437,9 +443,9 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
 }
 
 pafft_status launch(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
-                    const void* ghat, const void* mul, double scale, cudaStream_t st) {
-    return p->prec == 0 ? launch_t<double>(p, d, src, dst, batch, ghat, mul, scale, st)
-                        : launch_t<float>(p, d, src, dst, batch, ghat, mul, scale, st);
+                    const void* ghat, const void* mul, double scale, cudaStream_t st, long long grid_cap = 0) {
+    return p->prec == 0 ? launch_t<double>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap)
+                        : launch_t<float>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap);
 }
 
 // ---------------------------------------------------- helper kernels --
@@ -477,6 +483,39 @@ __global__ void scale_convert_kernel(const double2* __restrict__ in, cplx<T>* __
         const double2 v = in[i];
         if (out) out[i] = cplx<T>{(T)v.x, (T)v.y};
         out_scaled[i] = cplx<T>{(T)(v.x * s), (T)(v.y * s)};
+    }
+}
+
+// ghat_kernel[b*R + sum_j d_j wt(j)] = s * ghat[b*R + sum_j rev_{F_j}(d_j) wt(j)]:
+// the CONV pass multiplies frequency slots in its own natural-digit order.
+struct SlotPerm {
+    int radix, ns, R;
+    int F[4], wt[4];
+};
+
+__device__ __forceinline__ int rev_rt(int d, int radix, int f) {
+    int o = 0;
+    for (int p = 1; p < f; p *= radix) {
+        o = o * radix + d % radix;
+        d /= radix;
+    }
+    return o;
+}
+
+template <typename T>
+__global__ void kernel_ghat_kernel(const cplx<T>* __restrict__ in, cplx<T>* __restrict__ out, double s,
+                                   unsigned long long n, SlotPerm sp) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long blk = i / sp.R;
+        int rem = (int)(i - blk * sp.R), src = 0;
+        for (int j = 0; j < sp.ns; ++j) {
+            const int d = rem / sp.wt[j];
+            rem -= d * sp.wt[j];
+            src += rev_rt(d, sp.radix, sp.F[j]) * sp.wt[j];
+        }
+        const cplx<T> v = in[blk * sp.R + src];
+        out[i] = cplx<T>{(T)(v.x * s), (T)(v.y * s)};
     }
 }
 
@@ -718,6 +757,9 @@ pafft_status pafft_plan_create(unsigned radix, const size_t* dims, int rank, int
         p->rev_dev.push_back((uint32_t*)d);
     }
     for (auto& s : p->streams) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (auto& s : p->work) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
+    for (auto& e : p->join) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // table uploads above used pageable cudaMemcpy; make them visible to
     // every stream (including non-blocking ones) before the plan is used
     CUDA_TRY(cudaDeviceSynchronize());
@@ -730,6 +772,11 @@ pafft_status pafft_plan_destroy(pafft_plan_t plan) {
     cudaSetDevice(plan->device);
     for (auto& s : plan->streams)
         if (s) cudaStreamDestroy(s);
+    for (auto& s : plan->work)
+        if (s) cudaStreamDestroy(s);
+    if (plan->fork) cudaEventDestroy(plan->fork);
+    for (auto& e : plan->join)
+        if (e) cudaEventDestroy(e);
     delete plan;
     return PAFFT_OK;
 }
@@ -761,8 +808,8 @@ pafft_status pafft_plan_describe(pafft_plan_t p, char* buf, size_t len) {
     for (const auto& d : ps) {
         char line[256];
         snprintf(line, sizeof line,
-                 "%s axis=%d stages=[%d,%d) R=%d(%dx%dx%d) K0=%lld L=%lld C=%lld %s W=%d NT=%d smem=%zu ext=%d\n",
-                 kn[d.kind], d.axis, d.a, d.a + d.s, d.R, d.R1, d.R2, d.R3, d.K0, d.L, d.C,
+                 "%s axis=%d stages=[%d,%d) R=%d(%dx%dx%dx%d) K0=%lld L=%lld C=%lld %s W=%d NT=%d smem=%zu ext=%d\n",
+                 kn[d.kind], d.axis, d.a, d.a + d.s, d.R, d.F[0], d.F[1], d.F[2], d.F[3], d.K0, d.L, d.C,
                  d.contig ? "contig" : "strided", d.W, d.NT, d.smem, d.ext);
         s += line;
     }
@@ -799,12 +846,28 @@ pafft_status pafft_filter_sync_scaled(pafft_filter_t f, void* stream) {
     ST_TRY(set_device(p));
     cudaStream_t st = (cudaStream_t)stream;
     const double s = 1.0 / (double)p->total;
+    SlotPerm sp;
+    memset(&sp, 0, sizeof sp);
+    sp.radix = (int)p->radix;
+    sp.R = 1;
+    sp.ns = 0;
+    if (!p->pf.empty()) {
+        const PassDesc& cv = p->pf[p->pf.size() / 2];  // the CONV pass
+        sp.R = cv.R;
+        sp.ns = cv.nsteps;
+        int w = 1;
+        for (int j = cv.nsteps - 1; j >= 0; --j) {
+            sp.F[j] = cv.F[j];
+            sp.wt[j] = w;
+            w *= cv.F[j];
+        }
+    }
     if (p->prec == 0)
-        scale_kernel<double><<<grid_for(p->total, 256), 256, 0, st>>>((const double2*)f->ghat->p,
-                                                                       (double2*)f->ghat_scaled->p, s, p->total);
+        kernel_ghat_kernel<double><<<grid_for(p->total, 256), 256, 0, st>>>(
+            (const double2*)f->ghat->p, (double2*)f->ghat_scaled->p, s, p->total, sp);
     else
-        scale_kernel<float><<<grid_for(p->total, 256), 256, 0, st>>>((const float2*)f->ghat->p,
-                                                                      (float2*)f->ghat_scaled->p, s, p->total);
+        kernel_ghat_kernel<float><<<grid_for(p->total, 256), 256, 0, st>>>(
+            (const float2*)f->ghat->p, (float2*)f->ghat_scaled->p, s, p->total, sp);
     CUDA_TRY(cudaGetLastError());
     ++g_launches;
     return PAFFT_OK;
@@ -855,15 +918,16 @@ pafft_status pafft_prepare_filter_split(pafft_plan_t p, const double* g_re, cons
         ++g_launches;
         ++g_perm_passes;
     }
-    const double s = 1.0 / (double)n;
     if (p->prec == 0)
-        scale_convert_kernel<double><<<grid_for(n, 256), 256>>>((const double2*)gh64.p, (double2*)f->ghat->p,
-                                                                (double2*)f->ghat_scaled->p, s, n);
-    else
+        CUDA_TRY(cudaMemcpy(f->ghat->p, gh64.p, n * 16, cudaMemcpyDeviceToDevice));
+    else {
         scale_convert_kernel<float><<<grid_for(n, 256), 256>>>((const double2*)gh64.p, (float2*)f->ghat->p,
-                                                               (float2*)f->ghat_scaled->p, s, n);
-    CUDA_TRY(cudaGetLastError());
-    ++g_launches;
+                                                               (float2*)f->ghat_scaled->p, 1.0, n);
+        CUDA_TRY(cudaGetLastError());
+        ++g_launches;
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
+    ST_TRY(pafft_filter_sync_scaled(f, nullptr));
     CUDA_TRY(cudaDeviceSynchronize());
     *out = guard.release();
     return PAFFT_OK;
@@ -920,6 +984,15 @@ void* pafft_filter_device_ghat_scaled(pafft_filter_t f) { return f ? f->ghat_sca
 int pafft_filter_matches(pafft_filter_t f, pafft_plan_t p) { return f && p && key_match(f, p) ? 1 : 0; }
 
 // ------------------------------------------------------------- hot path
+// Signals per L2-resident chunk: all passes of a chunk run back to back so the
+// intermediate passes hit L2 (126 MB) instead of HBM; two chunks are in
+// flight on two internal streams, next to the resident filter.
+static size_t chunk_signals(pafft_plan_t p) {
+    const size_t sig = p->total * p->esize;
+    const size_t budget = (size_t)env_int("PAFFT_CHUNK_MB", 36) << 20;
+    return std::max<size_t>(1, budget / std::max<size_t>(sig, 1));
+}
+
 pafft_status pafft_convolve_permfree_oop(pafft_plan_t p, pafft_filter_t f, const void* x_dev, void* y_dev,
                                          size_t batch, void* stream) {
     if (!p || !f) return fail(PAFFT_INVALID_ARGUMENT, "null plan or filter");
@@ -930,9 +1003,38 @@ pafft_status pafft_convolve_permfree_oop(pafft_plan_t p, pafft_filter_t f, const
     cudaStream_t st = (cudaStream_t)stream;
     const std::vector<PassDesc>& ps = p->pf;
     if (ps.empty()) return hadamard_dev(p, x_dev, f->ghat_scaled->p, y_dev, batch, st);
-    for (size_t i = 0; i < ps.size(); ++i)
-        ST_TRY(launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch,
-                      ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr, nullptr, 1.0, st));
+    const size_t chunk = chunk_signals(p);
+    // measured on B200 (config 2): one-chunk launches lose more to tails than
+    // L2 residency saves, so the chunk pipeline is opt-in (PAFFT_PIPELINE=1)
+    const bool pipeline = ps.size() > 1 && batch > chunk && env_int("PAFFT_PIPELINE", 0) != 0;
+    if (!pipeline) {
+        for (size_t i = 0; i < ps.size(); ++i)
+            ST_TRY(launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch,
+                          ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr, nullptr, 1.0, st));
+        return PAFFT_OK;
+    }
+    // fork: both work streams wait for everything already queued on `st`
+    CUDA_TRY(cudaEventRecord(p->fork, st));
+    for (auto& w : p->work) CUDA_TRY(cudaStreamWaitEvent(w, p->fork, 0));
+    const size_t sig = p->total * p->esize;
+    int k = 0;
+    for (size_t done = 0; done < batch; done += chunk, ++k) {
+        const size_t nb = std::min(chunk, batch - done);
+        cudaStream_t w = p->work[k & 1];
+        const char* xs = (const char*)x_dev + done * sig;
+        char* ys = (char*)y_dev + done * sig;
+        for (size_t i = 0; i < ps.size(); ++i) {
+            // half the resident CTA slots each, so the two chunks run side by side
+            const long long cap = std::max<long long>(1, ps[i].max_ctas / 2);
+            ST_TRY(launch(p, ps[i], i == 0 ? (const void*)xs : (const void*)ys, ys, nb,
+                          ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr, nullptr, 1.0, w, cap));
+        }
+    }
+    // join
+    for (int i = 0; i < 2; ++i) {
+        CUDA_TRY(cudaEventRecord(p->join[i], p->work[i]));
+        CUDA_TRY(cudaStreamWaitEvent(st, p->join[i], 0));
+    }
     return PAFFT_OK;
 }
 
@@ -949,6 +1051,11 @@ pafft_status pafft_convolve_permfree_pass(pafft_plan_t p, pafft_filter_t f, cons
     ST_TRY(set_device(p));
     return launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch, ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr,
                   nullptr, 1.0, (cudaStream_t)stream);
+}
+
+size_t pafft_plan_chunk_signals(pafft_plan_t p) {
+    if (!p) return 0;
+    return env_int("PAFFT_PIPELINE", 0) != 0 ? chunk_signals(p) : 0;  // 0: whole batch per launch
 }
 
 pafft_status pafft_plan_pass_info(pafft_plan_t p, int i, int* kind, int* axis, int* R, int* stages) {

@@ -55,10 +55,11 @@ template <typename T> struct PassArgs {
     unsigned ext_bits;
     const cplx<T>* ext_lo;   // w_K0^{e},           e < 2^bits
     const cplx<T>* ext_hi;   // w_K0^{h * 2^bits},  h < ceil(K0 / 2^bits)
-    // internal twiddles
-    const cplx<T>* tw1;      // [k1][m23] = w_R^{k1 m23}
-    const cplx<T>* tw2;      // [k2][m3]  = w_{R2 R3}^{k2 m3}
-    // CONV filter (digit-reversed, pre-scaled by 1/N) and signal period
+    // internal twiddles of step i (i < nsteps - 1): tw[i][k * Q_i + lo] =
+    // w_{P_i}^{k lo}, P_i = R_i ... R_last, Q_i = P_i / R_i
+    const cplx<T>* tw[3];
+    // CONV filter (pre-scaled by 1/N, each R-block in the pass's slot order:
+    // see pafft_b200.cu kernel_ghat) and signal period
     const cplx<T>* ghat;
     long long N;
     // DIT epilogue: natural-order multiplier (period N) and/or scale
@@ -81,30 +82,36 @@ template <int RADIX, int P> __host__ __device__ constexpr int revd(int k) {
     return o;
 }
 
-template <int R1, int R2, int R3> struct Shape {
-    static constexpr int R = R1 * R2 * R3;
-    static constexpr int R23 = R2 * R3;
-    static constexpr int NSTEP = 1 + (R2 > 1 ? 1 : 0) + (R3 > 1 ? 1 : 0);
-    static constexpr int G1 = R23;       // step 1 groups: m23
-    static constexpr int G2 = R1 * R3;   // step 2 groups: (k1, m3)
-    static constexpr int G3 = R1 * R2;   // step 3 groups: (k1, k2)
+// Codelet split R = F0 * F1 * F2 * F3 (trailing 1s unused).  Step i works on
+// digit i of the row index m = sum_i m_i wt(i), wt(i) = F_{i+1} ... F_last:
+// groups are all combinations of the other digits, G(i) = R / F_i of them.
+template <int F0, int F1, int F2, int F3> struct Fac {
+    static constexpr int NS = 1 + (F1 > 1) + (F2 > 1) + (F3 > 1);
+    static constexpr int R = F0 * F1 * F2 * F3;
+    static constexpr int f(int i) { return i == 0 ? F0 : i == 1 ? F1 : i == 2 ? F2 : F3; }
+    // P(i) = F_i ... F_last;  wt(i) = Q(i) = P(i + 1)
+    static constexpr int P(int i) { return i >= NS ? 1 : f(i) * P(i + 1); }
+    static constexpr int Q(int i) { return P(i + 1); }
+    static constexpr int G(int i) { return R / f(i); }
+    // product F_0 ... F_{i-1} (weight of digit i in the frequency index)
+    static constexpr int L(int i) { return i == 0 ? 1 : L(i - 1) * f(i - 1); }
     static constexpr int gmin() {
-        int g = G1;
-        if (NSTEP >= 2 && G2 < g) g = G2;
-        if (NSTEP == 3 && G3 < g) g = G3;
+        int g = G(0);
+        for (int i = 1; i < NS; ++i)
+            if (G(i) < g) g = G(i);
         return g;
     }
     static constexpr int GMIN = gmin();
+    static constexpr int FMAX = R / GMIN;
 };
 
 // Compile-time tile policy shared by kernels and host plan (registry).
-template <typename T, int R1, int R2, int R3, int MAP> struct TilePolicy {
-    using S = Shape<R1, R2, R3>;
+template <typename T, typename FAC, int MAP> struct TilePolicy {
     static constexpr int ESZ = (int)sizeof(cplx<T>);
     static constexpr int SMEM_BUDGET = 110 * 1024;  // per tile buffer (two are resident)
     // STRIDED: 8 (fp64) / 16 (fp32) columns = one 128-byte row segment; more
-    // columns for single-codelet passes (no shared memory, tiny groups).
-    static constexpr int MAXW = MAP == MAP_STRIDED ? (S::NSTEP == 1 ? 64 : (ESZ == 16 ? 8 : 16)) : 64;
+    // columns for single-codelet passes (no shared-memory exchange).
+    static constexpr int MAXW = MAP == MAP_STRIDED ? (FAC::NS == 1 ? 64 : (ESZ == 16 ? 8 : 16)) : 64;
     // fp32 strided rows may start 8 bytes off a 16-byte boundary (odd C):
     // each shared row then holds W + 2 slots and the data sits at a per-row
     // shift of 0 or 1 element (see stage_tile).
@@ -112,25 +119,32 @@ template <typename T, int R1, int R2, int R3, int MAP> struct TilePolicy {
     static constexpr int rowslots(int w) { return SHIFT ? w + 2 : w; }
     static constexpr int wcalc() {
         int w = MAXW;
-        while (w > 1 && S::GMIN * w > 512) --w;
+        // STRIDED tiles keep the full 128-byte row (tensor-map boxes must land
+        // 128-byte aligned); up to 1024 threads per CTA.
+        while (w > 1 && FAC::GMIN * w > (MAP == MAP_STRIDED && FAC::NS > 1 ? 1024 : 512))
+            w = MAP == MAP_STRIDED ? w / 2 : w - 1;
         if (MAP == MAP_CONTIG)
-            while (w > 1 && S::GMIN * w > 256) --w;
-        while (w > 1 && S::R * rowslots(w) * ESZ > SMEM_BUDGET) --w;
+            while (w > 1 && FAC::GMIN * w > 256) --w;
+        while (w > 1 && FAC::R * rowslots(w) * ESZ > SMEM_BUDGET) --w;
         // at least one full warp: warp 0 issues the bulk copies
-        while (S::GMIN * w < 32 && S::R * rowslots(w + 1) * ESZ <= SMEM_BUDGET) ++w;
+        while (FAC::GMIN * w < 32 && FAC::R * rowslots(w + 1) * ESZ <= SMEM_BUDGET) ++w;
         if (SHIFT && (w & 1)) ++w;  // even W keeps rows 16-byte sized
         // fp32 contiguous tiles start at first*R elements: even W keeps every
         // tile start 16-byte aligned for the bulk copy
-        if (MAP == MAP_CONTIG && ESZ == 8 && (w & 1)) w = (w > 1 && S::R * (w + 1) * ESZ > SMEM_BUDGET) ? w - 1 : w + 1;
+        if (MAP == MAP_CONTIG && ESZ == 8 && (w & 1))
+            w = (w > 1 && FAC::R * (w + 1) * ESZ > SMEM_BUDGET) ? w - 1 : w + 1;
         return w;
     }
     static constexpr int W = wcalc();
     static constexpr int SW = rowslots(W);  // shared row stride (STRIDED)
-    static constexpr int NT = S::GMIN * W;
+    static constexpr int NT = FAC::GMIN * W;
     static_assert(NT >= 32, "tile policy needs a full warp");
     // two tile buffers (TMA double buffering) + two mbarriers
-    static constexpr int BUF = ((MAP == MAP_STRIDED ? S::R * SW : S::R * W) * ESZ + 15) / 16 * 16;
+    static constexpr int BUF = ((MAP == MAP_STRIDED ? FAC::R * SW : FAC::R * W) * ESZ + 15) / 16 * 16;
     static constexpr int SMEM = 2 * BUF + 16;
+    // resident CTAs per SM the shared memory allows (registers are capped to match)
+    static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024);
+    static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > 4 ? 4 : MINB_SMEM);
 };
 
 template <typename T>
@@ -270,19 +284,34 @@ __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorM
 // Persistent pass kernel: each CTA walks tiles blockIdx.x + i * gridDim.x.
 // Tile i+1 streams into the other shared buffer (TMA, mbarrier) while tile i
 // is transformed in place in its buffer; results go straight from registers
-// to global memory in their final order (rev-ordered rows for DIF).
-template <typename T, int RADIX, int R1, int R2, int R3, int KIND, int MAP>
-__global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT, 1)
+// to global memory in their final order (digit-reversed rows for DIF).
+//
+// DIF step i (i = 0 .. NS-1): group g = hi * Q_i + lo (hi: digits 0..i-1,
+// already frequency; lo: digits i+1.., still spatial); DFT_{F_i} over digit
+// i at slots hi * P_i + r * Q_i + lo; then twiddle w_{P_i}^{k lo} (i < last).
+// The last step holds frequency k = kf_hi + (R / F_last) * k_last with
+// position pos(k) = sum_j rev(k_j) wt(j): DIF stores it there (times the
+// external twiddle w_K0^{jj k}); CONV multiplies by ghat[pos] and turns round.
+// DIT step i (i = NS-1 .. 0) is the transpose: DFT over digit i (frequency ->
+// space), then twiddle w_{P_{i-1}}^{k_{i-1} (m Q_i + lo)} with conj for A-bar.
+// DIT kinds read the staged tile in its digit-reversed row order, so digit j
+// of a frequency index sits at rev(k_j) wt(j); CONV continues from the DIF's
+// natural frequency slots.  Every step reads and writes one slot set (in
+// place); the final spatial rows go to global memory with the epilogue.
+template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP>
+__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
+                                  TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::MINB)
     pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap) {
     using V = cplx<T>;
-    using Sh = Shape<R1, R2, R3>;
-    using Pol = TilePolicy<T, R1, R2, R3, MAP>;
-    constexpr int R = Sh::R, R23 = Sh::R23, NSTEP = Sh::NSTEP, GMIN = Sh::GMIN;
+    using FA = Fac<F0, F1, F2, F3>;
+    using Pol = TilePolicy<T, FA, MAP>;
+    constexpr int R = FA::R, NS = FA::NS, GMIN = FA::GMIN;
     constexpr int W = Pol::W;
     constexpr int SW = Pol::SW;
     constexpr int BUFE = Pol::BUF / (int)sizeof(V);  // elements per tile buffer
     constexpr bool STRIDED = MAP == MAP_STRIDED;
     constexpr bool SHIFT = Pol::SHIFT;
+    constexpr int FL = FA::f(NS - 1);  // last codelet
     extern __shared__ __align__(128) unsigned char smem_raw[];
     V* const bufs = reinterpret_cast<V*>(smem_raw);
     unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem_raw + 2 * Pol::BUF);
@@ -322,6 +351,7 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT, 1)
         const int b0 = SHIFT && !a.use_tmap ? (int)(geo.base & 1) : 0;
         auto sref = [&](int row) -> V& { return scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)]; };
         V* __restrict__ gdst = a.dst + geo.base + (STRIDED ? c : (long long)c * R);
+        // external twiddle base/step for this column: w_K0^{jj kf}, w_K0^{jj S}
         auto ext_pair = [&](int kf, int S, V& tw, V& st) {
             const unsigned long long jj = (unsigned long long)(first + c) / a.sq;
             tw = ext_root(a, jj * (unsigned long long)kf);
@@ -329,244 +359,151 @@ __global__ void __launch_bounds__(TilePolicy<T, R1, R2, R3, MAP>::NT, 1)
         };
         mbar_wait(&bars[b], (it >> 1) & 1);
 
+        // hi index (digits 0..I-1 of a group) -> frequency offset sum k_j L(j)
+        // and digit-reversed slot offset sum rev(k_j) wt(j); `rev_in` says the
+        // slot digits are already reversed (DIT kinds).
+        auto hi_decode = [&](auto Ic, int hi, bool rev_in, int& kf, int& pos) {
+            constexpr int I = decltype(Ic)::value;
+            kf = 0;
+            pos = 0;
+            static_for<0, I>([&](auto jc) {
+                constexpr int jj = I - 1 - decltype(jc)::value;  // least significant digit first
+                constexpr int fj = FA::f(jj);
+                const int d = hi % fj;
+                hi /= fj;
+                const int k = rev_in ? revd<RADIX, fj>(d) : d;
+                kf += k * FA::L(jj);
+                pos += (rev_in ? d : revd<RADIX, fj>(d)) * FA::Q(jj);
+            });
+        };
+
         if constexpr (KIND == KIND_DIF || KIND == KIND_CONV) {
-            // ------------------------------------------------ DIF step 1
+            static_for<0, NS>([&](auto Ic) {
+                constexpr int I = decltype(Ic)::value;
+                constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
+                if constexpr (I > 0) __syncthreads();
 #pragma unroll
-            for (int j = 0; j < Sh::G1 / GMIN; ++j) {
-                const int g = gt + j * GMIN;  // m23
-                V z[R1];
-#pragma unroll
-                for (int m1 = 0; m1 < R1; ++m1) z[m1] = sref(m1 * R23 + g);
-                dft<R1, 1>(z);
-                if constexpr (NSTEP == 1) {
-                    if constexpr (KIND == KIND_DIF) {
-                        if (ok) {
-                            V tw{1, 0}, st{1, 0};
-                            if (a.ext) ext_pair(0, 1, tw, st);
-#pragma unroll
-                            for (int k1 = 0; k1 < R1; ++k1) {
-                                gdst[(long long)revd<RADIX, R1>(k1) * rs] = a.ext ? cmul(z[k1], tw) : z[k1];
-                                if (a.ext) tw = cmul(tw, st);
-                            }
-                        }
-                    } else {  // CONV with a single codelet: x ghat, inverse, store
-                        if (ok) {
-                            const V* gh = a.ghat + ((first + c) % (a.N / R)) * (long long)R;
-#pragma unroll
-                            for (int k1 = 0; k1 < R1; ++k1) z[k1] = cmul(z[k1], __ldg(gh + revd<RADIX, R1>(k1)));
-                            dft<R1, -1>(z);
-#pragma unroll
-                            for (int m1 = 0; m1 < R1; ++m1) gdst[(long long)m1 * rs] = z[m1];
-                        }
-                    }
-                } else {
-                    const V* tw1 = a.tw1 + g;
-#pragma unroll
-                    for (int k1 = 1; k1 < R1; ++k1) z[k1] = cmul(z[k1], __ldg(tw1 + k1 * R23));
-#pragma unroll
-                    for (int k1 = 0; k1 < R1; ++k1) sref(k1 * R23 + g) = z[k1];
-                }
-            }
-            if constexpr (NSTEP >= 2) {
-                __syncthreads();
-                // -------------------------------------------- DIF step 2
-#pragma unroll
-                for (int j = 0; j < Sh::G2 / GMIN; ++j) {
+                for (int j = 0; j < FA::G(I) / GMIN; ++j) {
                     const int g = gt + j * GMIN;
-                    const int k1 = g / R3, m3 = g - (g / R3) * R3;
-                    const int sb = k1 * R23 + m3;
-                    V z[R2];
+                    const int hi = g / QI, lo = g - (g / QI) * QI;
+                    const int sb = hi * PI + lo;
+                    V z[FI];
 #pragma unroll
-                    for (int m2 = 0; m2 < R2; ++m2) z[m2] = sref(sb + m2 * R3);
-                    dft<R2, 1>(z);
-                    if constexpr (NSTEP == 2) {
-                        const int pfix = revd<RADIX, R1>(k1) * R23;
+                    for (int m = 0; m < FI; ++m) z[m] = sref(sb + m * QI);
+                    dft<FI, 1>(z);
+                    if constexpr (I < NS - 1) {
+                        const V* tw = a.tw[I] + lo;
+#pragma unroll
+                        for (int k = 1; k < FI; ++k) z[k] = cmul(z[k], __ldg(tw + k * QI));
+#pragma unroll
+                        for (int k = 0; k < FI; ++k) sref(sb + k * QI) = z[k];
+                    } else {
+                        // last DIF step (QI == 1, lo == 0): frequency kf + (R/FL) k
+                        int kf, pos;
+                        hi_decode(Ic, hi, false, kf, pos);
                         if constexpr (KIND == KIND_DIF) {
                             if (ok) {
                                 V tw{1, 0}, st{1, 0};
-                                if (a.ext) ext_pair(k1, R1, tw, st);
-                                V* gp = gdst + (long long)pfix * rs;
+                                if (a.ext) ext_pair(kf, R / FL, tw, st);
+                                V* gp = gdst + (long long)pos * rs;
 #pragma unroll
-                                for (int k2 = 0; k2 < R2; ++k2) {
-                                    gp[(long long)revd<RADIX, R2>(k2) * rs] = a.ext ? cmul(z[k2], tw) : z[k2];
+                                for (int k = 0; k < FI; ++k) {
+                                    gp[(long long)revd<RADIX, FI>(k) * rs] = a.ext ? cmul(z[k], tw) : z[k];
                                     if (a.ext) tw = cmul(tw, st);
                                 }
                             }
-                        } else {  // CONV: x ghat, DIT-conj step B (in registers), back to smem
+                        } else {
+                            // CONV: x ghat (digit-reversed, 1/N folded in), then the
+                            // first DIT-conj step on the same registers
                             if (ok) {
-                                const V* gh = a.ghat + ((first + c) % (a.N / R)) * (long long)R + pfix;
+                                // the kernel copy of ghat is stored in this pass's slot
+                                // order (ghat[pos(k)] at slot sum k_j wt(j)): coalesced
+                                const V* gh = a.ghat + ((first + c) % (a.N / R)) * (long long)R + sb;
 #pragma unroll
-                                for (int k2 = 0; k2 < R2; ++k2) z[k2] = cmul(z[k2], __ldg(gh + revd<RADIX, R2>(k2)));
+                                for (int k = 0; k < FI; ++k) z[k] = cmul(z[k], __ldg(gh + k));
                             }
-                            dft<R2, -1>(z);
-                            const V* tw1 = a.tw1 + k1 * R23;
+                            dft<FI, -1>(z);
+                            if constexpr (NS == 1) {
+                                if (ok) {
 #pragma unroll
-                            for (int m2 = 1; m2 < R2; ++m2) z[m2] = cmulc(z[m2], __ldg(tw1 + m2));
+                                    for (int m = 0; m < FI; ++m) gdst[(long long)m * rs] = z[m];
+                                }
+                            } else {
+                                // twiddle of DIF step NS-2, conjugated: k_{NS-2} (m * 1 + 0)
+                                constexpr int FP = FA::f(NS - 2), QP = FA::Q(NS - 2);
+                                const int kp = hi % FP;
+                                const V* tw = a.tw[NS - 2] + kp * QP;
 #pragma unroll
-                            for (int m2 = 0; m2 < R2; ++m2) sref(sb + m2) = z[m2];
-                        }
-                    } else {
-                        const V* tw2 = a.tw2 + m3;
+                                for (int m = 1; m < FI; ++m) z[m] = cmulc(z[m], __ldg(tw + m));
 #pragma unroll
-                        for (int k2 = 1; k2 < R2; ++k2) z[k2] = cmul(z[k2], __ldg(tw2 + k2 * R3));
-#pragma unroll
-                        for (int k2 = 0; k2 < R2; ++k2) sref(sb + k2 * R3) = z[k2];
-                    }
-                }
-            }
-            if constexpr (NSTEP == 3) {
-                __syncthreads();
-                // -------------------------------------------- DIF step 3
-#pragma unroll
-                for (int j = 0; j < Sh::G3 / GMIN; ++j) {
-                    const int g = gt + j * GMIN;
-                    const int k1 = g / R2, k2 = g - (g / R2) * R2;
-                    const int sb = k1 * R23 + k2 * R3;
-                    V z[R3];
-#pragma unroll
-                    for (int m3 = 0; m3 < R3; ++m3) z[m3] = sref(sb + m3);
-                    dft<R3, 1>(z);
-                    const int pfix = revd<RADIX, R1>(k1) * R23 + revd<RADIX, R2>(k2) * R3;
-                    if constexpr (KIND == KIND_DIF) {
-                        if (ok) {
-                            V tw{1, 0}, st{1, 0};
-                            if (a.ext) ext_pair(k1 + R1 * k2, R1 * R2, tw, st);
-                            V* gp = gdst + (long long)pfix * rs;
-#pragma unroll
-                            for (int k3 = 0; k3 < R3; ++k3) {
-                                gp[(long long)revd<RADIX, R3>(k3) * rs] = a.ext ? cmul(z[k3], tw) : z[k3];
-                                if (a.ext) tw = cmul(tw, st);
+                                for (int m = 0; m < FI; ++m) sref(sb + m) = z[m];
                             }
                         }
-                    } else {  // CONV: x ghat, DIT-conj step A
-                        if (ok) {
-                            const V* gh = a.ghat + ((first + c) % (a.N / R)) * (long long)R + pfix;
-#pragma unroll
-                            for (int k3 = 0; k3 < R3; ++k3) z[k3] = cmul(z[k3], __ldg(gh + revd<RADIX, R3>(k3)));
-                        }
-                        dft<R3, -1>(z);
-                        if (k2 != 0) {
-                            const V* tw2 = a.tw2 + k2 * R3;
-#pragma unroll
-                            for (int m3 = 1; m3 < R3; ++m3) z[m3] = cmulc(z[m3], __ldg(tw2 + m3));
-                        }
-#pragma unroll
-                        for (int m3 = 0; m3 < R3; ++m3) sref(sb + m3) = z[m3];
                     }
                 }
-            }
+            });
         }
 
         if constexpr (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ || KIND == KIND_CONV) {
             constexpr int S = (KIND == KIND_DIT_FWD) ? 1 : -1;
-            constexpr bool FIRST = KIND != KIND_CONV;  // DIT kinds start from the staged input
+            constexpr bool FIRST = KIND != KIND_CONV;  // slots hold digit-reversed frequency digits
             auto tw = [](V x, V w) -> V { return S > 0 ? cmul(x, w) : cmulc(x, w); };
-            // ---------------------------------------- DIT step A (R3 > 1)
-            if constexpr (NSTEP == 3 && FIRST) {
+            // DIT steps I = NS-1 .. 0 (CONV already did NS-1 in registers)
+            static_for<0, NS>([&](auto Rc) {
+                constexpr int I = NS - 1 - decltype(Rc)::value;
+                constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
+                if constexpr (!(KIND == KIND_CONV && I == NS - 1)) {
+                    if constexpr (KIND == KIND_CONV || I < NS - 1) __syncthreads();
 #pragma unroll
-                for (int j = 0; j < Sh::G3 / GMIN; ++j) {
-                    const int g = gt + j * GMIN;
-                    const int k1 = g / R2, k2 = g - (g / R2) * R2;
-                    const int pfix = revd<RADIX, R1>(k1) * R23 + revd<RADIX, R2>(k2) * R3;
-                    V z[R3];
+                    for (int j = 0; j < FA::G(I) / GMIN; ++j) {
+                        const int g = gt + j * GMIN;
+                        const int hi = g / QI, lo = g - (g / QI) * QI;
+                        const int sb = hi * PI + lo;
+                        V z[FI];
 #pragma unroll
-                    for (int k3 = 0; k3 < R3; ++k3) z[k3] = sref(pfix + revd<RADIX, R3>(k3));
-                    if (a.ext && ok) {
-                        V w, st;
-                        ext_pair(k1 + R1 * k2, R1 * R2, w, st);
+                        for (int k = 0; k < FI; ++k) z[k] = sref(sb + (FIRST ? revd<RADIX, FI>(k) : k) * QI);
+                        if constexpr (FIRST && I == NS - 1) {
+                            // pre-twiddle w_K0^{+-jj k} on the first DIT step
+                            if (a.ext && ok) {
+                                int kf, pos;
+                                hi_decode(std::integral_constant<int, I>{}, hi, true, kf, pos);
+                                V w, st;
+                                ext_pair(kf, R / FL, w, st);
 #pragma unroll
-                        for (int k3 = 0; k3 < R3; ++k3) {
-                            z[k3] = tw(z[k3], w);
-                            w = cmul(w, st);
+                                for (int k = 0; k < FI; ++k) {
+                                    z[k] = tw(z[k], w);
+                                    w = cmul(w, st);
+                                }
+                            }
                         }
-                    }
-                    dft<R3, S>(z);
-                    if (k2 != 0) {
-                        const V* tw2 = a.tw2 + k2 * R3;
+                        dft<FI, S>(z);
+                        if constexpr (I > 0) {
+                            constexpr int FP = FA::f(I - 1), QP = FA::Q(I - 1);
+                            const int dp = hi % FP;
+                            const int kp = FIRST ? revd<RADIX, FP>(dp) : dp;
+                            const V* twp = a.tw[I - 1] + kp * QP + lo;
 #pragma unroll
-                        for (int m3 = 1; m3 < R3; ++m3) z[m3] = tw(z[m3], __ldg(tw2 + m3));
-                    }
-                    // in place: the rows pfix + rev(k3) just read are rows pfix + m3
+                            for (int m = 0; m < FI; ++m)
+                                if (m != 0 || lo != 0) z[m] = tw(z[m], __ldg(twp + m * QI));
 #pragma unroll
-                    for (int m3 = 0; m3 < R3; ++m3) sref(pfix + m3) = z[m3];
-                }
-            }
-            // ---------------------------------------- DIT step B (R2 > 1)
-            // Slot convention: DIT kinds keep the staged (digit-reversed) row
-            // order, so group k1 lives at rev(k1)*R23 and index k2 at rev(k2)*R3;
-            // CONV continues from the DIF's natural frequency slots.  Every step
-            // then reads and writes the same slot set (in place).
-            if constexpr (NSTEP >= 2 && !(KIND == KIND_CONV && NSTEP == 2)) {
-                if constexpr (NSTEP == 3) __syncthreads();
+                            for (int m = 0; m < FI; ++m) sref(sb + m * QI) = z[m];
+                        } else if (ok) {
+                            // final spatial rows m * Q_0 + lo (hi == 0)
+                            V* gp = gdst + (long long)lo * rs;
 #pragma unroll
-                for (int j = 0; j < Sh::G2 / GMIN; ++j) {
-                    const int g = gt + j * GMIN;
-                    const int k1 = g / R3, m3 = g - (g / R3) * R3;
-                    const int sk1 = FIRST ? revd<RADIX, R1>(k1) : k1;
-                    const int sb = sk1 * R23 + m3;
-                    V z[R2];
-#pragma unroll
-                    for (int k2 = 0; k2 < R2; ++k2) z[k2] = sref(sb + (FIRST ? revd<RADIX, R2>(k2) : k2) * R3);
-                    if constexpr (NSTEP == 2 && FIRST) {
-                        if (a.ext && ok) {
-                            V w, st;
-                            ext_pair(k1, R1, w, st);
-#pragma unroll
-                            for (int k2 = 0; k2 < R2; ++k2) {
-                                z[k2] = tw(z[k2], w);
-                                w = cmul(w, st);
+                            for (int m = 0; m < FI; ++m) {
+                                V y = z[m];
+                                if (a.mul) {
+                                    const long long e = (gp - a.dst) + (long long)(m * QI) * rs;
+                                    y = cmul(y, __ldg(a.mul + (e % a.N)));
+                                }
+                                if (a.has_scale) y = V{y.x * a.scale, y.y * a.scale};
+                                gp[(long long)(m * QI) * rs] = y;
                             }
                         }
                     }
-                    dft<R2, S>(z);
-                    const V* tw1 = a.tw1 + k1 * R23 + m3;
-#pragma unroll
-                    for (int m2 = 0; m2 < R2; ++m2)
-                        if (m2 * R3 != 0 || m3 != 0) z[m2] = tw(z[m2], __ldg(tw1 + m2 * R3));
-#pragma unroll
-                    for (int m2 = 0; m2 < R2; ++m2) sref(sb + m2 * R3) = z[m2];
                 }
-            }
-            // ---------------------------------------- DIT step C (always)
-            if constexpr (!(KIND == KIND_CONV && NSTEP == 1)) {
-                if constexpr (NSTEP >= 2) __syncthreads();
-#pragma unroll
-                for (int j = 0; j < Sh::G1 / GMIN; ++j) {
-                    const int g = gt + j * GMIN;  // m23
-                    V z[R1];
-                    if constexpr (NSTEP == 1) {
-#pragma unroll
-                        for (int k1 = 0; k1 < R1; ++k1) z[k1] = sref(revd<RADIX, R1>(k1));
-                        if (a.ext && ok) {
-                            V w, st;
-                            ext_pair(0, 1, w, st);
-#pragma unroll
-                            for (int k1 = 0; k1 < R1; ++k1) {
-                                z[k1] = tw(z[k1], w);
-                                w = cmul(w, st);
-                            }
-                        }
-                    } else {
-#pragma unroll
-                        for (int k1 = 0; k1 < R1; ++k1)
-                            z[k1] = sref((FIRST ? revd<RADIX, R1>(k1) : k1) * R23 + g);
-                    }
-                    dft<R1, S>(z);
-                    if (ok) {
-                        V* gp = gdst + (long long)g * rs;
-#pragma unroll
-                        for (int m1 = 0; m1 < R1; ++m1) {
-                            V y = z[m1];
-                            if (a.mul) {
-                                const long long e = (gp - a.dst) + (long long)(m1 * R23) * rs;
-                                y = cmul(y, __ldg(a.mul + (e % a.N)));
-                            }
-                            if (a.has_scale) y = V{y.x * a.scale, y.y * a.scale};
-                            gp[(long long)(m1 * R23) * rs] = y;
-                        }
-                    }
-                }
-            }
+            });
         }
         // all reads of this buffer are done: refill it with tile it + 2
         __syncthreads();

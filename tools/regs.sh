@@ -13,5 +13,5 @@ for line in sys.stdin:
     if m2: sp=(int(m2.group(1)), int(m2.group(2)))
     m=re.search(r'Used (\d+) registers',line)
     if m and cur:
-        a=re.findall(r'Li(\d+)E',cur); print('r%s R=%s kind=%s map=%s regs=%s spill=%s' % (a[0], 'x'.join(a[1:4]), a[4], a[5], m.group(1), sp)); cur=None
+        a=re.findall(r'Li(\d+)E',cur); print('r%s R=%s kind=%s map=%s regs=%s spill=%s' % (a[0], 'x'.join(a[1:5]), a[5], a[6], m.group(1), sp)); cur=None
 "
