@@ -221,4 +221,18 @@ template <int P, int S, typename V> __device__ __forceinline__ void dft(V (&z)[P
     }
 }
 
+// z[k] *= w^(k) for k = 1 .. F-1 (S = -1: conj(w)^k), w^k built by binary
+// powering in registers (error ~ log2(F) roundings) instead of F-1 table loads.
+template <int F, int S, typename V> __device__ __forceinline__ void twiddle_powers(V (&z)[F], V w) {
+    if constexpr (F > 1) {
+        if constexpr (S < 0) w.y = -w.y;
+        V p[F];
+        p[1] = w;
+#pragma unroll
+        for (int k = 2; k < F; ++k) p[k] = (k & 1) ? cmul(p[k - 1], p[1]) : cmul(p[k / 2], p[k / 2]);
+#pragma unroll
+        for (int k = 1; k < F; ++k) z[k] = cmul(z[k], p[k]);
+    }
+}
+
 }  // namespace pafft_b200

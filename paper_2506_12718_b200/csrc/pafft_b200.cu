@@ -85,10 +85,10 @@ const KernelEntry* find_kernel(int prec, int radix, int R, int kind, int map) {
     return nullptr;
 }
 
-int max_stages_compiled(int radix) {
+int max_stages_compiled(int prec, int radix, int kind, int map) {
     int best = 0;
     for (const auto& e : registry()) {
-        if (e.radix != radix || e.prec != 0) continue;
+        if (e.radix != radix || e.prec != prec || e.kind != kind || e.map != map) continue;
         int s = 0;
         for (int v = e.R; v > 1; v /= radix) ++s;
         best = std::max(best, s);
@@ -270,9 +270,9 @@ int env_int(const char* name, int dflt) {
 // transposes).  Strided axes first (any order is valid: modes commute,
 // SPEC.md:226), then axis 0 split so its last group is a contiguous block.
 void build_groups(pafft_plan_t p) {
-    const int maxs = max_stages_compiled((int)p->radix);
+    const int maxs = max_stages_compiled(p->prec, (int)p->radix, KIND_CONV, MAP_CONTIG);
     const int max_mid = std::min(maxs, env_int("PAFFT_MAX_MID_STAGES", maxs));
-    int max_str = maxs;
+    int max_str = max_stages_compiled(p->prec, (int)p->radix, KIND_DIF, MAP_STRIDED);
     if (p->radix == 2) max_str = std::min(max_str, 11);
     max_str = std::min(max_str, env_int("PAFFT_MAX_STRIDED_STAGES", max_str));
     p->groups.clear();

@@ -392,9 +392,8 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                     for (int m = 0; m < FI; ++m) z[m] = sref(sb + m * QI);
                     dft<FI, 1>(z);
                     if constexpr (I < NS - 1) {
-                        const V* tw = a.tw[I] + lo;
-#pragma unroll
-                        for (int k = 1; k < FI; ++k) z[k] = cmul(z[k], __ldg(tw + k * QI));
+                        // w_{P_I}^{k lo}: powers of tw[I][Q_I + lo] = w_{P_I}^{lo}
+                        twiddle_powers<FI, 1>(z, __ldg(a.tw[I] + QI + lo));
 #pragma unroll
                         for (int k = 0; k < FI; ++k) sref(sb + k * QI) = z[k];
                     } else {
@@ -429,12 +428,6 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                                     for (int m = 0; m < FI; ++m) gdst[(long long)m * rs] = z[m];
                                 }
                             } else {
-                                // twiddle of DIF step NS-2, conjugated: k_{NS-2} (m * 1 + 0)
-                                constexpr int FP = FA::f(NS - 2), QP = FA::Q(NS - 2);
-                                const int kp = hi % FP;
-                                const V* tw = a.tw[NS - 2] + kp * QP;
-#pragma unroll
-                                for (int m = 1; m < FI; ++m) z[m] = cmulc(z[m], __ldg(tw + m));
 #pragma unroll
                                 for (int m = 0; m < FI; ++m) sref(sb + m) = z[m];
                             }
@@ -476,15 +469,10 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                                 }
                             }
                         }
+                        // pre-twiddle: the transpose of DIF step I's w_{P_I}^{k lo}
+                        if constexpr (I < NS - 1) twiddle_powers<FI, S>(z, __ldg(a.tw[I] + QI + lo));
                         dft<FI, S>(z);
                         if constexpr (I > 0) {
-                            constexpr int FP = FA::f(I - 1), QP = FA::Q(I - 1);
-                            const int dp = hi % FP;
-                            const int kp = FIRST ? revd<RADIX, FP>(dp) : dp;
-                            const V* twp = a.tw[I - 1] + kp * QP + lo;
-#pragma unroll
-                            for (int m = 0; m < FI; ++m)
-                                if (m != 0 || lo != 0) z[m] = tw(z[m], __ldg(twp + m * QI));
 #pragma unroll
                             for (int m = 0; m < FI; ++m) sref(sb + m * QI) = z[m];
                         } else if (ok) {
