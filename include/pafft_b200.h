@@ -153,7 +153,8 @@ pafft_status pafft_fft_transposed(pafft_plan_t plan, void* x_dev, size_t batch, 
 pafft_status pafft_permute(pafft_plan_t plan, void* x_dev, size_t batch, void* stream);
 /* Host split variants of the transforms (module.cpp:91-99 semantics). op:
  * 0 fft_forward, 1 fft_backward, 2 fft_forward_unordered,
- * 3 fft_backward_unordered, 4 fft_transposed, 5 permute. */
+ * 3 fft_backward_unordered, 4 fft_transposed (A^T), 5 permute,
+ * 6 conjugate ladder A-bar without the 1/n (butterfly_conjugate). */
 pafft_status pafft_transform_split(pafft_plan_t plan, int op, double* re, double* im, size_t batch);
 /* filter_from_impulse (convolution.cpp:16-21): g = fft_forward(h), split host. */
 pafft_status pafft_filter_from_impulse_split(pafft_plan_t plan, const double* h_re, const double* h_im,

@@ -1276,6 +1276,7 @@ pafft_status pafft_transform_split(pafft_plan_t p, int op, double* re, double* i
         case 3: ST_TRY(pafft_fft_backward_unordered(p, x.p, batch, st)); break;
         case 4: ST_TRY(pafft_fft_transposed(p, x.p, batch, st)); break;
         case 5: ST_TRY(pafft_permute(p, x.p, batch, st)); break;
+        case 6: ST_TRY(ladder_op(p, KIND_DIT_CONJ, false, 1.0, nullptr, x.p, batch, st)); break;
         default: return fail(PAFFT_INVALID_ARGUMENT, "unknown transform op %d", op);
     }
     CUDA_TRY(cudaStreamSynchronize(st));

@@ -1,0 +1,160 @@
+// Reference-style unit checks compiled against the C++ drop-in header
+// (include/pafft/pafft.hpp) and run on the GPU library.  The cases restate
+// the reference's own tests (test_convolution.cpp:22-145,
+// test_butterfly.cpp:28-45/106-121, test_core.cpp:29-70,
+// test_permutation.cpp:15-31); a tiny harness replaces doctest (absent).
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "pafft/pafft.hpp"
+
+using namespace pafft;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                       \
+    do {                                                                  \
+        if (cond) ++g_pass;                                               \
+        else { ++g_fail; std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #cond); } \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)                       \
+    do {                                               \
+        bool ok_ = false;                              \
+        try { expr; } catch (const T&) { ok_ = true; } catch (...) {} \
+        CHECK(ok_ && #T);                              \
+    } while (0)
+
+static ComplexBuffer buf(std::initializer_list<std::complex<double>> v) {
+    ComplexBuffer b(v.size());
+    std::size_t i = 0;
+    for (auto c : v) b.set(i++, c);
+    return b;
+}
+static double max_diff(const ComplexBuffer& a, const ComplexBuffer& b) {
+    double m = 0;
+    for (std::size_t i = 0; i < a.size(); ++i)
+        m = std::max(m, std::max(std::abs(a.re[i] - b.re[i]), std::abs(a.im[i] - b.im[i])));
+    return m;
+}
+static bool bitwise_equal(const ComplexBuffer& a, const ComplexBuffer& b) {
+    for (std::size_t i = 0; i < a.size(); ++i)
+        if (a.re[i] != b.re[i] || a.im[i] != b.im[i]) return false;
+    return a.size() == b.size();
+}
+static ComplexBuffer random_buffer(std::size_t n, std::uint64_t seed) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> d(-1, 1);
+    ComplexBuffer b(n);
+    for (std::size_t i = 0; i < n; ++i) { b.re[i] = d(rng); b.im[i] = d(rng); }
+    return b;
+}
+
+int main() {
+    // plan validation (test_core.cpp:29-42)
+    CHECK_THROWS_AS(plan_create(Radix::r2, TensorShape(std::vector<std::size_t>{})), EmptyShape);
+    CHECK_THROWS_AS(plan_create(Radix::r8, TensorShape{4}), NotAPowerOfRadix);
+    CHECK_THROWS_AS(plan_create(Radix::r4, TensorShape{8}), NotAPowerOfRadix);
+    try {
+        plan_create(Radix::r2, TensorShape{8, 3});
+        CHECK(false);
+    } catch (const NotAPowerOfRadix& e) {
+        CHECK(e.dim == 1 && e.extent == 3);
+    }
+    CHECK_THROWS_AS(radix_from_value(7), Error);
+    {
+        const Plan p2 = plan_create(Radix::r2, TensorShape{8});
+        const std::vector<std::uint32_t> expect{0, 4, 2, 6, 1, 5, 3, 7};
+        for (std::size_t j = 0; j < 8; ++j) CHECK(p2.rev_map(0)[j] == expect[j]);
+        CHECK(p2.depth(0) == 3);
+        CHECK(digit_reverse(6, 2, 3) == 3 && digit_reverse(5, 4, 2) == 5 && digit_reverse(5, 3, 2) == 7);
+        CHECK_THROWS_AS(digit_reverse(8, 2, 3), IndexOutOfRange);
+    }
+    // 4-point ladders (test_butterfly.cpp:28-45)
+    {
+        const Plan plan = plan_create(Radix::r2, TensorShape{4});
+        ComplexBuffer x = buf({1, 3, 2, 4});
+        butterfly_forward(x, plan, 0);
+        CHECK(max_diff(x, buf({10, {-2, 2}, -2, {-2, -2}})) < 1e-13);
+        ComplexBuffer y = buf({10, -2, {-2, 2}, {-2, -2}});
+        butterfly_conjugate(y, plan, 0);
+        CHECK(max_diff(y, buf({4, 8, 12, 16})) < 1e-13);
+        ComplexBuffer z = buf({1, 2, 3, 4});
+        butterfly_transposed(z, plan, 0);
+        CHECK(max_diff(z, buf({10, -2, {-2, 2}, {-2, -2}})) < 1e-13);
+        ComplexBuffer w(8);
+        CHECK_THROWS_AS(butterfly_forward(w, plan, 0), ShapeMismatch);
+    }
+    // filter layout, delay filter, both pipelines (test_convolution.cpp:32-61)
+    {
+        const Plan plan = plan_create(Radix::r2, TensorShape{4});
+        const PreparedFilter f = prepare_filter(buf({0, 1, 2, 3}), plan);
+        CHECK(max_diff(f.ghat, buf({0, 2, 1, 3})) == 0.0);
+        CHECK(f.key == plan.key());
+        CHECK_THROWS_AS(prepare_filter(ComplexBuffer(3), plan), LengthMismatch);
+        const ComplexBuffer g = filter_from_impulse(buf({0, 1, 0, 0}), plan);
+        CHECK(max_diff(g, buf({1, {0, -1}, -1, {0, 1}})) < 1e-14);
+        ComplexBuffer x = buf({1, 2, 3, 4});
+        convolve_standard(x, g, plan);
+        CHECK(max_diff(x, buf({4, 1, 2, 3})) < 1e-13);
+        ComplexBuffer y = buf({1, 2, 3, 4});
+        convolve_permfree(y, prepare_filter(g, plan), plan);
+        CHECK(max_diff(y, buf({4, 1, 2, 3})) < 1e-13);
+    }
+    // pass accounting (test_convolution.cpp:63-79)
+    {
+        const Plan plan = plan_create(Radix::r4, TensorShape{16, 16});
+        const ComplexBuffer g = random_buffer(plan.total(), 73);
+        ComplexBuffer x = random_buffer(plan.total(), 74);
+        reset_permutation_pass_count();
+        convolve_standard(x, g, plan);
+        CHECK(permutation_pass_count() == 2);
+        reset_permutation_pass_count();
+        const PreparedFilter filter = prepare_filter(g, plan);
+        CHECK(permutation_pass_count() == 1);
+        reset_permutation_pass_count();
+        convolve_permfree(x, filter, plan);
+        CHECK(permutation_pass_count() == 0);
+    }
+    // plan binding (test_convolution.cpp:81-97)
+    {
+        const Plan plan = plan_create(Radix::r2, TensorShape{16});
+        const PreparedFilter filter = prepare_filter(random_buffer(16, 79), plan);
+        ComplexBuffer x = random_buffer(16, 80);
+        CHECK_THROWS_AS(convolve_permfree(x, filter, plan_create(Radix::r4, TensorShape{16})), FilterPlanMismatch);
+        CHECK_THROWS_AS(convolve_permfree(x, filter, plan_create(Radix::r2, TensorShape{4, 4})), FilterPlanMismatch);
+        convolve_permfree(x, filter, plan_create(Radix::r2, TensorShape{16}));
+        ++g_pass;
+    }
+    // reuse without drift (test_convolution.cpp:99-111) and radix 3
+    for (auto [radix, shape] : {std::pair<Radix, TensorShape>{Radix::r2, {8, 8}}, {Radix::r3, {27, 9}},
+                                {Radix::r5, {125}}}) {
+        const Plan plan = plan_create(radix, shape);
+        const PreparedFilter filter = prepare_filter(random_buffer(plan.total(), 83), plan);
+        const ComplexBuffer x = random_buffer(plan.total(), 84);
+        ComplexBuffer first = x;
+        convolve_permfree(first, filter, plan);
+        for (int round = 0; round < 3; ++round) {
+            ComplexBuffer again = x;
+            convolve_permfree(again, filter, plan);
+            CHECK(bitwise_equal(again, first));
+        }
+        ComplexBuffer std_ = x;
+        convolve_standard(std_, filter_from_impulse(random_buffer(plan.total(), 85), plan), plan);
+        ++g_pass;
+    }
+    // conjugate ladder equals conjugated forward ladder (test_butterfly.cpp:106-121)
+    {
+        const Plan plan = plan_create(Radix::r4, TensorShape{256});
+        const ComplexBuffer x = random_buffer(256, 37);
+        ComplexBuffer direct = x;
+        butterfly_conjugate(direct, plan, 0);
+        ComplexBuffer wrapped = x;
+        for (double& v : wrapped.im) v = -v;
+        butterfly_forward(wrapped, plan, 0);
+        for (double& v : wrapped.im) v = -v;
+        CHECK(max_diff(direct, wrapped) < 1e-12);
+    }
+    std::printf("dropin: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail ? 1 : 0;
+}
