@@ -352,6 +352,7 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
         for (int v = 1; v <= 256 && v <= d.R; ++v)
             if (d.R % v == 0) rb = v;
         d.rb = rb;
+        if (d.R / rb > 256) d.use_tmap = 0;
     }
     d.ext = d.L > 1;
     if (d.ext) ST_TRY(ext_table(p, d.K0, d));
@@ -388,12 +389,14 @@ pafft_status tensor_map(pafft_plan_t p, const PassDesc& d, const void* src, size
     }
     auto enc = encode_fn();
     if (!enc) return fail(PAFFT_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
-    const cuuint64_t dims[2] = {(cuuint64_t)(2 * d.C), (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)(d.C * p->esize)};
-    const cuuint32_t box[2] = {(cuuint32_t)(2 * d.sw), (cuuint32_t)d.rb};
-    const cuuint32_t estr[2] = {1, 1};
+    // 3-D view {2C reals, rb rows, (rows / rb) row groups}: one box = one tile
+    const unsigned long long nb = (unsigned long long)(d.R / d.rb);
+    const cuuint64_t dims[3] = {(cuuint64_t)(2 * d.C), (cuuint64_t)d.rb, (cuuint64_t)(rows / d.rb)};
+    const cuuint64_t strides[2] = {(cuuint64_t)(d.C * p->esize), (cuuint64_t)(d.rb * d.C * p->esize)};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * d.sw), (cuuint32_t)d.rb, (cuuint32_t)nb};
+    const cuuint32_t estr[3] = {1, 1, 1};
     CUtensorMap m;
-    const CUresult r = enc(&m, p->prec == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+    const CUresult r = enc(&m, p->prec == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                            const_cast<void*>(src), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -118,11 +118,17 @@ template <typename T, typename FAC, int MAP> struct TilePolicy {
     static constexpr bool SHIFT = MAP == MAP_STRIDED && ESZ == 8;
     static constexpr int rowslots(int w) { return SHIFT ? w + 2 : w; }
     static constexpr int wcalc() {
+        if (MAP == MAP_STRIDED && FAC::NS > 1) {
+            // powers of two up to one 128-byte row segment (measured on B200:
+            // full 128-byte rows beat 64-byte rows with twice the residency)
+            int w = MAXW;
+            while (w > 1 && 2 * FAC::R * rowslots(w) * ESZ > 220 * 1024) w /= 2;
+            while (w > 1 && FAC::GMIN * w > 1024) w /= 2;
+            if (SHIFT && (w & 1)) ++w;
+            return w;
+        }
         int w = MAXW;
-        // STRIDED tiles keep the full 128-byte row (tensor-map boxes must land
-        // 128-byte aligned); up to 1024 threads per CTA.
-        while (w > 1 && FAC::GMIN * w > (MAP == MAP_STRIDED && FAC::NS > 1 ? 1024 : 512))
-            w = MAP == MAP_STRIDED ? w / 2 : w - 1;
+        while (w > 1 && FAC::GMIN * w > 512) --w;
         if (MAP == MAP_CONTIG)
             while (w > 1 && FAC::GMIN * w > 256) --w;
         while (w > 1 && FAC::R * rowslots(w) * ESZ > SMEM_BUDGET) --w;
@@ -140,7 +146,8 @@ template <typename T, typename FAC, int MAP> struct TilePolicy {
     static constexpr int NT = FAC::GMIN * W;
     static_assert(NT >= 32, "tile policy needs a full warp");
     // two tile buffers (TMA double buffering) + two mbarriers
-    static constexpr int BUF = ((MAP == MAP_STRIDED ? FAC::R * SW : FAC::R * W) * ESZ + 15) / 16 * 16;
+    // (tensor-map destinations must be 128-byte aligned)
+    static constexpr int BUF = ((MAP == MAP_STRIDED ? FAC::R * SW : FAC::R * W) * ESZ + 127) / 128 * 128;
     static constexpr int SMEM = 2 * BUF + 16;
     // resident CTAs per SM the shared memory allows (registers are capped to match)
     static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024);
@@ -220,12 +227,12 @@ __device__ __forceinline__ TileGeo tile_geo(const PassArgs<T>& a, long long tile
 // aligned addresses and sizes: fp64 always satisfies this; fp32 rows copy the
 // enclosing 16-byte-aligned window (shift_j = 1 when the row starts 8 bytes
 // into it), and an odd fp32 contiguous tail element is moved by one thread.
-__device__ __forceinline__ void tma_load_2d(void* sdst, const CUtensorMap* map, int x, int y,
+__device__ __forceinline__ void tma_load_3d(void* sdst, const CUtensorMap* map, int x, int y, int z,
                                             unsigned long long* bar) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
             smem_u32(sdst)),
-        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -235,14 +242,12 @@ __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorM
     using V = cplx<T>;
     const TileGeo g = tile_geo<R, W, STRIDED>(a, tile);
     if (STRIDED && a.use_tmap) {
-        // boxes of rb rows x SW columns (out-of-range columns zero-filled);
-        // the tile lands densely as [row][SW]
+        // one 3-D box {SW columns, rb rows, R/rb row groups} = the whole tile,
+        // landing densely as [row][SW] (out-of-range columns zero-filled)
         if (lane == 0) {
             const long long p = tile / a.tiles_per_panel;
-            const int nb = R / a.rb;
             mbar_expect_tx(bar, (unsigned)(R * SW * sizeof(V)));
-            for (int i = 0; i < nb; ++i)
-                tma_load_2d(buf + i * a.rb * SW, map, (int)(2 * g.first), (int)(p * R + i * a.rb), bar);
+            tma_load_3d(buf, map, (int)(2 * g.first), 0, (int)(p * (R / a.rb)), bar);
         }
     } else if (STRIDED) {
         const V* src = a.src + g.base;
