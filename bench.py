@@ -238,14 +238,15 @@ def main():
     else:
         filt = pf.empty_filter(plan)
     if world > 1:
-        dist.broadcast(pf.filter_device_tensor(filt), src=0)
-        dist.broadcast(pf.filter_device_tensor(filt, scaled=True), src=0)
+        from paper_2506_12718_b200 import dist as pdist
+        pdist.broadcast_filter_tensors([pf.filter_device_tensor(filt), pf.filter_device_tensor(filt, scaled=True)])
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t_prep
 
     # ---- inputs: per-rank shard (fixed per-GPU batch), resident in HBM
+    from paper_2506_12718_b200 import dist as pdist
     per = args.batch or (cfg.calls if cfg.calls > 1 else cfg.batch)
-    first = rank * per
+    first, per = pdist.shard(per, rank)
     host = torch.empty((per, N), dtype=cdt, pin_memory=True)
     hv = host.numpy()
     if prec == pf.F64:
@@ -314,11 +315,7 @@ def main():
     if world > 1:
         dist.barrier()
     launches = pf.kernel_launch_count() - launches0
-    ms = e0.elapsed_time(e1)
-    t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
-    ms_max = float(t_ms.item())
+    ms_max = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
     # keep the GPU busy (untimed) until the clock sampler has >= 1 s of samples
     t_soak = time.time()
     while time.time() - tw0 < 1.2 and time.time() - t_soak < 3.0:
@@ -375,11 +372,7 @@ def main():
         t = time.perf_counter()
         for _ in range(ysteps):
             host_step()
-        et = time.perf_counter() - t
-        t_e = torch.tensor([et], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-        et = float(t_e.item())
+        et = pdist.max_over_ranks(time.perf_counter() - t, dev)
         e2e = {"value": per * world * ysteps / et, "unit": "conv/s", "h2d_bytes_per_step": per * S,
                "d2h_bytes_per_step": per * S, "steps": ysteps, "pipelined": "3 streams, 64 MiB chunks, pinned"}
 

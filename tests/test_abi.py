@@ -1,0 +1,143 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads and exports every
+entry point include/pafft_b200.h declares; the Python mirror exposes the
+reference module's names (python/pafft/__init__.py) with its error contract
+(RuntimeError subclasses, module.cpp / README.md:138-143); host-only pieces
+(digit reversal, cost models, workload generators) match the reference and
+the oracle.  No GPU compute is called here."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pafft_b200.h")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(pafft_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(os.path.join(ROOT, "paper_2506_12718_b200", "libpafft_b200.so"))
+    syms = declared_symbols()
+    assert len(syms) >= 40
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_header():
+    from paper_2506_12718_b200 import _lib
+    assert set(declared_symbols()) <= set(_lib.EXPORTED)
+
+
+def test_mirror_exposes_reference_module_names():
+    import paper_2506_12718_b200 as pf
+    reference_all = ["Plan", "PreparedFilter", "convolve_permfree", "convolve_standard", "digit_reverse",
+                     "estimate_ai", "estimate_flop", "fft_backward", "fft_backward_unordered", "fft_forward",
+                     "fft_forward_unordered", "filter_from_impulse", "prepare_filter"]
+    for name in reference_all:
+        assert hasattr(pf, name), name
+    for cls in ("NotAPowerOfRadix", "EmptyShape", "LengthMismatch", "ShapeMismatch", "FilterPlanMismatch",
+                "IndexOutOfRange"):
+        assert issubclass(getattr(pf, cls), RuntimeError)
+
+
+def test_plan_validation_contract_without_gpu():
+    """test_core.cpp:29-42 / test_smoke.py:61-67: validation happens before any
+    device work, so the error contract holds on a CPU-only host."""
+    import paper_2506_12718_b200 as pf
+    with pytest.raises(pf.EmptyShape):
+        pf.Plan(2, [])
+    with pytest.raises(pf.NotAPowerOfRadix) as e:
+        pf.Plan(2, [8, 3])
+    assert (e.value.dim, e.value.extent) == (1, 3)
+    with pytest.raises(pf.NotAPowerOfRadix):
+        pf.Plan(8, [4])
+    with pytest.raises(pf.NotAPowerOfRadix):
+        pf.Plan(2, [0])
+    with pytest.raises(RuntimeError):
+        pf.Plan(7, [49])
+    with pytest.raises(RuntimeError):
+        pf.Plan(2, [24])
+
+
+def test_no_cpu_fallback_without_device():
+    """The product path fails loudly instead of computing on the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2506_12718_b200 as pf
+    with pytest.raises(pf.NoDevice):
+        pf.Plan(3, [27])
+
+
+def test_digit_reverse_known_answers():
+    """test_permutation.cpp:15-24 / test_smoke.py:72-76."""
+    import paper_2506_12718_b200 as pf
+    assert pf.digit_reverse(6, 2, 3) == 3
+    assert pf.digit_reverse(5, 4, 2) == 5
+    assert pf.digit_reverse(0, 8, 4) == 0
+    assert pf.digit_reverse(1, 2, 3) == 4
+    assert pf.digit_reverse(7, 8, 1) == 7
+    assert pf.digit_reverse(5, 3, 2) == 7
+    assert [pf.digit_reverse(j, 2, 3) for j in range(8)] == [0, 4, 2, 6, 1, 5, 3, 7]
+    with pytest.raises(pf.IndexOutOfRange):
+        pf.digit_reverse(8, 2, 3)
+    with pytest.raises(pf.IndexOutOfRange):
+        pf.digit_reverse(1, 2, 0)
+
+
+def test_cost_models():
+    """test_smoke.py:79-82 and test_bench.cpp:24-45."""
+    import paper_2506_12718_b200 as pf
+    assert pf.estimate_flop(1 << 20, 2) == 104857600.0
+    assert abs(pf.estimate_ai(4096, 4, True) - 0.265625) < 1e-12
+    assert pf.estimate_ai(4096, 4, False) < pf.estimate_ai(4096, 4, True)
+    assert abs(pf.estimate_ai(4096, 2, True) - 0.15625) < 1e-12
+    assert pf.estimate_flop(1, 2) == 0.0
+
+
+def test_workload_generators_match_oracle_bitwise(orc):
+    """SplitMix64 (bench.cpp:22-49) + Box-Muller: product generator == oracle's."""
+    import paper_2506_12718_b200 as pf
+    for seed in (0x5EED5EED5EED5EED + 1, 12345, 0):
+        assert np.array_equal(pf.fill_uniform(seed, 1000), orc.fill_uniform(seed, 1000))
+        assert np.array_equal(pf.fill_normal(seed, 1000), orc.fill_normal(seed, 1000))
+    u = pf.fill_uniform(7, 200000)
+    assert -1 <= u.real.min() and u.real.max() <= 1 and abs(u.real.mean()) < 0.01
+    z = pf.fill_normal(7, 200000)
+    assert abs(z.real.std() - 1) < 0.01 and abs(z.imag.mean()) < 0.01
+
+
+def test_splitmix_first_draw():
+    """bench.cpp:22-42: the first SplitMix64 output for seed 0 (public test vector)."""
+    import oracle
+    o = oracle.Oracle()
+    st = C.c_uint64(0)
+    assert o.L.orc_splitmix64_next(C.byref(st)) == 0xE220A8397B1DCDAF
+
+
+def test_workload_configs_match_baseline():
+    from paper_2506_12718_b200 import workload
+    c = workload.CONFIGS
+    assert c[1].dims == [1 << 20] and c[1].radix == 2 and c[1].calls == 100
+    assert c[2].dims == [3 ** 13] and c[2].radix == 3 and c[2].batch == 64
+    assert c[3].dims == [2048, 2048] and c[3].batch == 16
+    assert c[4].dims == [256] * 3 and c[4].radix == 4 and c[4].batch == 8
+    assert c[5].dims == [5 ** 7] and c[5].batch == 4096
+    # B_alg = 2S + S/B_g
+    assert abs(workload.bytes_per_conv(c[1]) - 33.72e6) / 33.72e6 < 2e-3
+    assert abs(workload.bytes_per_conv(c[2]) - 51.42e6) / 51.42e6 < 2e-3
+
+
+def test_filters_of_configs_3_and_4():
+    from paper_2506_12718_b200 import workload
+    h3 = workload.impulse(workload.CONFIGS[3])
+    assert abs(h3.sum() - 1) < 1e-12 and np.all(h3.imag == 0)
+    assert h3.real.argmax() == 0 and abs(h3[1] - h3[2047]) < 1e-18  # circular symmetry
+    h4 = workload.impulse(workload.CONFIGS[4])
+    assert h4[0] == 1.0 and abs(h4[1] - np.exp(-1 / 16)) < 1e-15
