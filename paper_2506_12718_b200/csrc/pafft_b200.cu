@@ -280,7 +280,20 @@ void build_groups(pafft_plan_t p) {
         const int t = (int)p->depth[q];
         if (t == 0) continue;
         const int lim = (q == 0) ? std::max(max_mid, 1) : std::max(max_str, 1);
-        if (q == 0 && t > max_mid) {
+        const int forced_mid = env_int("PAFFT_MID_STAGES", 0);
+        if (q == 0 && forced_mid > 0 && forced_mid < t && forced_mid <= max_mid) {
+            // tuning override: contiguous group of exactly forced_mid stages,
+            // the rest split evenly into strided groups
+            const int rest = t - forced_mid;
+            const int npass = (rest + max_str - 1) / max_str;
+            int a = 0;
+            for (int i = 0; i < npass; ++i) {
+                const int s = rest / npass + (i >= npass - rest % npass ? 1 : 0);
+                p->groups.push_back({q, a, s});
+                a += s;
+            }
+            p->groups.push_back({q, a, forced_mid});
+        } else if (q == 0 && t > max_mid) {
             // outer strided groups, then the contiguous group (gets the remainder)
             const int npass = (t + std::min(max_mid, max_str) - 1) / std::min(max_mid, max_str);
             int a = 0;
