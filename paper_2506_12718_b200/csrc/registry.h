@@ -44,4 +44,4 @@ void register_r8_f32(Registry&);
 #define PAFFT_SHAPES_R3(X)                                                                                    \
     X(3, 3, 1, 1, 1) X(3, 9, 1, 1, 1) X(3, 27, 1, 1, 1) X(3, 9, 9, 1, 1) X(3, 9, 9, 3, 1) X(3, 9, 9, 9, 1)      \
     X(3, 9, 9, 9, 3) X(3, 9, 9, 9, 9)
-#define PAFFT_SHAPES_R5(X) X(5, 5, 1, 1, 1) X(5, 25, 1, 1, 1) X(5, 25, 5, 1, 1) X(5, 25, 25, 1, 1) X(5, 25, 25, 5, 1)
+#define PAFFT_SHAPES_R5(X) X(5, 5, 1, 1, 1) X(5, 25, 1, 1, 1) X(5, 5, 5, 5, 1) X(5, 5, 5, 5, 5) X(5, 25, 25, 5, 1)
