@@ -446,13 +446,17 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     a.scale = (T)scale;
     a.has_scale = scale != 1.0;
     if (a.tiles == 0) return PAFFT_OK;
-    CUtensorMap map;
+    CUtensorMap map, map_dst;
     memset(&map, 0, sizeof map);
+    memset(&map_dst, 0, sizeof map_dst);
     a.use_tmap = d.use_tmap;
     a.rb = d.rb;
-    if (d.use_tmap) ST_TRY(tensor_map(p, d, src, batch, &map));
+    if (d.use_tmap) {
+        ST_TRY(tensor_map(p, d, src, batch, &map));
+        ST_TRY(tensor_map(p, d, dst, batch, &map_dst));
+    }
     const long long grid = std::max<long long>(1, std::min<long long>(a.tiles, grid_cap > 0 ? std::min(grid_cap, d.max_ctas) : d.max_ctas));
-    void* args[] = {&a, &map};
+    void* args[] = {&a, &map, &map_dst};
     CUDA_TRY(cudaLaunchKernel(d.fn, dim3((unsigned)grid), dim3(d.NT), args, d.smem, st));
     ++g_launches;
     return PAFFT_OK;

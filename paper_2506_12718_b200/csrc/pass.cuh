@@ -236,6 +236,20 @@ __device__ __forceinline__ void tma_load_3d(void* sdst, const CUtensorMap* map, 
         : "memory");
 }
 
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* ssrc, int x, int y, int z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map),
+                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(ssrc))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store_1d(void* gdst, const void* ssrc, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 template <int R, int W, int SW, bool STRIDED, typename T>
 __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorMap* map, long long tile,
                                            cplx<T>* buf, unsigned long long* bar, int lane) {
@@ -306,7 +320,8 @@ __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorM
 template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP>
 __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                                   TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::MINB)
-    pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap) {
+    pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                const __grid_constant__ CUtensorMap tmap_dst) {
     using V = cplx<T>;
     using FA = Fac<F0, F1, F2, F3>;
     using Pol = TilePolicy<T, FA, MAP>;
@@ -317,6 +332,11 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
     constexpr bool STRIDED = MAP == MAP_STRIDED;
     constexpr bool SHIFT = Pol::SHIFT;
     constexpr int FL = FA::f(NS - 1);  // last codelet
+    // Results leave through shared memory and one bulk/tensor store per tile
+    // (scattered 128-byte STG rows reach ~2 TB/s on B200, bulk stores ~6);
+    // fp32 strided tiles (per-row shifted layout) keep register stores.
+    constexpr bool TSTORE = !SHIFT;
+    constexpr int NGL = FA::G(NS - 1) / GMIN;  // last-step groups per thread
     extern __shared__ __align__(128) unsigned char smem_raw[];
     V* const bufs = reinterpret_cast<V*>(smem_raw);
     unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem_raw + 2 * Pol::BUF);
@@ -382,6 +402,10 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
             });
         };
 
+        // DIF results of the last step, held until every thread has read its
+        // last-step inputs (the output rows pos(k) belong to other groups)
+        V zl[KIND == KIND_DIF ? NGL : 1][KIND == KIND_DIF ? FL : 1];
+        int pl[KIND == KIND_DIF ? NGL : 1];
         if constexpr (KIND == KIND_DIF || KIND == KIND_CONV) {
             static_for<0, NS>([&](auto Ic) {
                 constexpr int I = decltype(Ic)::value;
@@ -406,16 +430,14 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                         int kf, pos;
                         hi_decode(Ic, hi, false, kf, pos);
                         if constexpr (KIND == KIND_DIF) {
-                            if (ok) {
-                                V tw{1, 0}, st{1, 0};
-                                if (a.ext) ext_pair(kf, R / FL, tw, st);
-                                V* gp = gdst + (long long)pos * rs;
+                            V tw{1, 0}, st{1, 0};
+                            if (a.ext && ok) ext_pair(kf, R / FL, tw, st);
 #pragma unroll
-                                for (int k = 0; k < FI; ++k) {
-                                    gp[(long long)revd<RADIX, FI>(k) * rs] = a.ext ? cmul(z[k], tw) : z[k];
-                                    if (a.ext) tw = cmul(tw, st);
-                                }
+                            for (int k = 0; k < FI; ++k) {
+                                zl[j][k] = a.ext ? cmul(z[k], tw) : z[k];
+                                if (a.ext) tw = cmul(tw, st);
                             }
+                            pl[j] = pos;
                         } else {
                             // CONV: x ghat (digit-reversed, 1/N folded in), then the
                             // first DIT-conj step on the same registers
@@ -428,7 +450,10 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                             }
                             dft<FI, -1>(z);
                             if constexpr (NS == 1) {
-                                if (ok) {
+                                if constexpr (TSTORE) {
+#pragma unroll
+                                    for (int m = 0; m < FI; ++m) sref(m) = z[m];
+                                } else if (ok) {
 #pragma unroll
                                     for (int m = 0; m < FI; ++m) gdst[(long long)m * rs] = z[m];
                                 }
@@ -440,6 +465,21 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                     }
                 }
             });
+        }
+
+        if constexpr (KIND == KIND_DIF) {
+            if constexpr (TSTORE) {
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < NGL; ++j)
+#pragma unroll
+                    for (int k = 0; k < FL; ++k) sref(pl[j] + revd<RADIX, FL>(k)) = zl[j][k];
+            } else if (ok) {
+#pragma unroll
+                for (int j = 0; j < NGL; ++j)
+#pragma unroll
+                    for (int k = 0; k < FL; ++k) gdst[(long long)(pl[j] + revd<RADIX, FL>(k)) * rs] = zl[j][k];
+            }
         }
 
         if constexpr (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ || KIND == KIND_CONV) {
@@ -480,30 +520,59 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                         if constexpr (I > 0) {
 #pragma unroll
                             for (int m = 0; m < FI; ++m) sref(sb + m * QI) = z[m];
-                        } else if (ok) {
-                            // final spatial rows m * Q_0 + lo (hi == 0)
+                        } else {
+                            // final spatial rows m * Q_0 + lo (hi == 0), epilogue in registers
                             V* gp = gdst + (long long)lo * rs;
 #pragma unroll
                             for (int m = 0; m < FI; ++m) {
                                 V y = z[m];
-                                if (a.mul) {
+                                if (a.mul && ok) {
                                     const long long e = (gp - a.dst) + (long long)(m * QI) * rs;
                                     y = cmul(y, __ldg(a.mul + (e % a.N)));
                                 }
                                 if (a.has_scale) y = V{y.x * a.scale, y.y * a.scale};
-                                gp[(long long)(m * QI) * rs] = y;
+                                if constexpr (TSTORE) sref(sb + m * QI) = y;
+                                else if (ok) gp[(long long)(m * QI) * rs] = y;
                             }
                         }
                     }
                 }
             });
         }
-        // all reads of this buffer are done: refill it with tile it + 2
+        // the tile is final in shared memory: one bulk/tensor store, then (once
+        // the store has read the buffer) refill it with tile it + 2
         __syncthreads();
-        if (warp == 0 && tile + 2 * ts < a.tiles) {
-            fence_proxy_async();
-            stage_tile<R, W, SW, STRIDED>(a, &tmap, tile + 2 * ts, buf, &bars[b], lane);
+        if (warp == 0) {
+            if constexpr (TSTORE) {
+                if (lane == 0) {
+                    fence_proxy_async();
+                    if constexpr (STRIDED) {
+                        const long long p = tile / a.tiles_per_panel;
+                        tma_store_3d(&tmap_dst, buf, (int)(2 * first), 0, (int)(p * (R / a.rb)));
+                    } else {
+                        const long long n = (long long)geo.nvalid * R;
+                        unsigned bytes = (unsigned)(n * sizeof(V));
+                        if constexpr (sizeof(V) == 8) {
+                            if (bytes & 15u) {  // odd fp32 element count: tail by hand
+                                bytes -= 8u;
+                                a.dst[geo.base + n - 1] = buf[n - 1];
+                            }
+                        }
+                        if (bytes) bulk_store_1d(a.dst + geo.base, buf, bytes);
+                    }
+                    bulk_commit();
+                    bulk_wait_read0();
+                }
+                __syncwarp();
+            }
+            if (tile + 2 * ts < a.tiles) {
+                fence_proxy_async();
+                stage_tile<R, W, SW, STRIDED>(a, &tmap, tile + 2 * ts, buf, &bars[b], lane);
+            }
         }
+    }
+    if constexpr (TSTORE) {
+        if (t == 0) bulk_wait0();  // stores complete before the CTA retires
     }
 }
 
