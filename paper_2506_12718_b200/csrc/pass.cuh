@@ -363,12 +363,30 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
     }
     __syncthreads();  // hand-copied fp32 tail elements of the first tiles
 
+    // Deferred refill: after storing tile i from buffer b, the refill of b
+    // with tile i+2 waits for the store to drain shared memory; warp 0 does
+    // that after the next tile's first barrier instead of stalling the CTA.
+    long long pend = -1;
+    V* pbuf = nullptr;
+    unsigned long long* pbar = nullptr;
+    auto service = [&]() {
+        if (warp == 0 && pend >= 0) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            fence_proxy_async();
+            stage_tile<R, W, SW, STRIDED>(a, &tmap, pend, pbuf, pbar, lane);
+        }
+        pend = -1;
+    };
     int it = 0;
     for (long long tile = t0; tile < a.tiles; tile += ts, ++it) {
         const int b = it & 1;
         V* const buf = bufs + b * BUFE;
         const TileGeo geo = tile_geo<R, W, STRIDED>(a, tile);
         const long long first = geo.first;
+        // CONV: this column's filter block (the panel's position inside its signal)
+        const V* const gblk =
+            KIND == KIND_CONV ? a.ghat + (long long)((unsigned)(first + c) % (unsigned)(a.N / R)) * R : nullptr;
         const bool ok = c < geo.nvalid;
         V* const scol = STRIDED ? buf + c : buf + c * R;
         // shared element of tile row `row` for this thread's column
@@ -411,6 +429,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                 constexpr int I = decltype(Ic)::value;
                 constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
                 if constexpr (I > 0) __syncthreads();
+                if constexpr (I == 1) service();
 #pragma unroll
                 for (int j = 0; j < FA::G(I) / GMIN; ++j) {
                     const int g = gt + j * GMIN;
@@ -444,7 +463,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                             if (ok) {
                                 // the kernel copy of ghat is stored in this pass's slot
                                 // order (ghat[pos(k)] at slot sum k_j wt(j)): coalesced
-                                const V* gh = a.ghat + ((first + c) % (a.N / R)) * (long long)R + sb;
+                                const V* gh = gblk + sb;
 #pragma unroll
                                 for (int k = 0; k < FI; ++k) z[k] = cmul(z[k], __ldg(gh + k));
                             }
@@ -492,6 +511,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                 constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
                 if constexpr (!(KIND == KIND_CONV && I == NS - 1)) {
                     if constexpr (KIND == KIND_CONV || I < NS - 1) __syncthreads();
+                    if constexpr (KIND != KIND_CONV && I == NS - 2) service();
 #pragma unroll
                     for (int j = 0; j < FA::G(I) / GMIN; ++j) {
                         const int g = gt + j * GMIN;
@@ -561,16 +581,18 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                         if (bytes) bulk_store_1d(a.dst + geo.base, buf, bytes);
                     }
                     bulk_commit();
-                    bulk_wait_read0();
                 }
                 __syncwarp();
             }
-            if (tile + 2 * ts < a.tiles) {
-                fence_proxy_async();
-                stage_tile<R, W, SW, STRIDED>(a, &tmap, tile + 2 * ts, buf, &bars[b], lane);
-            }
         }
+        if (tile + 2 * ts < a.tiles) {
+            pend = tile + 2 * ts;
+            pbuf = buf;
+            pbar = &bars[b];
+        }
+        if constexpr (!TSTORE || NS == 1) service();  // no later barrier in the next tile
     }
+    service();
     if constexpr (TSTORE) {
         if (t == 0) bulk_wait0();  // stores complete before the CTA retires
     }
