@@ -126,6 +126,7 @@ struct PassDesc {
     size_t smem = 0;
     long long max_ctas = 1;
     int use_tmap = 0, rb = 0, sw = 0;  // STRIDED tensor-map staging
+    int swz = 0, swz_b1 = 0;           // CONTIG 128B-swizzled staging (power-of-two radix)
     int ext = 0;
     unsigned ext_bits = 0;
     const void* ext_lo = nullptr;
@@ -356,6 +357,14 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
         if (occ < 1) return fail(PAFFT_CUDA_ERROR, "pass kernel R=%d cannot be resident (smem %zu)", d.R, d.smem);
         d.max_ctas = (long long)occ * sms;
     }
+    if (d.contig && (p->radix == 2 || p->radix == 4 || p->radix == 8) && env_int("PAFFT_NO_SWIZZLE", 0) == 0) {
+        const long long tile_bytes = (long long)d.R * d.W * (long long)p->esize;
+        if (tile_bytes % 1024 == 0) {
+            const long long tr = tile_bytes / 128;
+            d.swz_b1 = (int)std::min<long long>(tr, 256);
+            d.swz = (tr % d.swz_b1 == 0 && tr / d.swz_b1 <= 256) ? 1 : 0;
+        }
+    }
     if (!d.contig) {
         // 2-D tensor map staging needs 16-byte row strides (always for fp64,
         // even C for fp32); otherwise one bulk copy per row.
@@ -421,6 +430,41 @@ pafft_status tensor_map(pafft_plan_t p, const PassDesc& d, const void* src, size
     return PAFFT_OK;
 }
 
+// Contiguous tiles as rows of 128 bytes, SWIZZLE_128B: 3-D view
+// {128 B of reals, b1 rows, row groups}; one box = one tile.
+pafft_status tensor_map_swz(pafft_plan_t p, const PassDesc& d, const void* src, size_t batch, CUtensorMap* out) {
+    const unsigned long long rows = (unsigned long long)p->total * batch * p->esize / 128;
+    char key[160];
+    snprintf(key, sizeof key, "swz/%p/%llu/%d/%d/%d", src, rows, d.R * d.W, d.swz_b1, p->prec);
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        auto it = p->tmaps.find(key);
+        if (it != p->tmaps.end()) {
+            *out = it->second;
+            return PAFFT_OK;
+        }
+    }
+    auto enc = encode_fn();
+    if (!enc) return fail(PAFFT_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    const unsigned long long tr = (unsigned long long)d.R * d.W * p->esize / 128;
+    const unsigned inner = p->prec == 0 ? 16u : 32u;  // reals per 128-byte row
+    const cuuint64_t dims[3] = {inner, (cuuint64_t)d.swz_b1, (cuuint64_t)(rows / d.swz_b1)};
+    const cuuint64_t strides[2] = {128, (cuuint64_t)128 * d.swz_b1};
+    const cuuint32_t box[3] = {inner, (cuuint32_t)d.swz_b1, (cuuint32_t)(tr / d.swz_b1)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap m;
+    const CUresult r = enc(&m, p->prec == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                           const_cast<void*>(src), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PAFFT_CUDA_ERROR, "cuTensorMapEncodeTiled (swizzled) failed (%d)", (int)r);
+    std::lock_guard<std::mutex> lk(p->mu);
+    if (p->tmaps.size() > 4096) p->tmaps.clear();
+    p->tmaps[key] = m;
+    *out = m;
+    return PAFFT_OK;
+}
+
 template <typename T>
 pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
                       const void* ghat, const void* mul, double scale, cudaStream_t st, long long grid_cap) {
@@ -451,9 +495,14 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     memset(&map_dst, 0, sizeof map_dst);
     a.use_tmap = d.use_tmap;
     a.rb = d.rb;
+    a.swz = d.swz && (a.panels % d.W == 0);
+    a.swz_b1 = d.swz_b1;
     if (d.use_tmap) {
         ST_TRY(tensor_map(p, d, src, batch, &map));
         ST_TRY(tensor_map(p, d, dst, batch, &map_dst));
+    } else if (a.swz) {
+        ST_TRY(tensor_map_swz(p, d, src, batch, &map));
+        ST_TRY(tensor_map_swz(p, d, dst, batch, &map_dst));
     }
     const long long grid = std::max<long long>(1, std::min<long long>(a.tiles, grid_cap > 0 ? std::min(grid_cap, d.max_ctas) : d.max_ctas));
     void* args[] = {&a, &map, &map_dst};

@@ -70,6 +70,11 @@ template <typename T> struct PassArgs {
     // bulk copy per row
     int use_tmap;
     int rb;
+    // CONTIG tiles of power-of-two radix: staged through a 128-byte-swizzled
+    // tensor map (rows of 128 B; 16-byte chunk index XOR row index), which
+    // removes the 8-way bank conflicts of power-of-two slot strides
+    int swz;
+    int swz_b1;   // box rows per row group
 };
 
 // Base-r digit reversal over the digits of P = r^s (permutation.cpp:27-37).
@@ -147,7 +152,8 @@ template <typename T, typename FAC, int MAP> struct TilePolicy {
     static_assert(NT >= 32, "tile policy needs a full warp");
     // two tile buffers (TMA double buffering) + two mbarriers
     // (tensor-map destinations must be 128-byte aligned)
-    static constexpr int BUF = ((MAP == MAP_STRIDED ? FAC::R * SW : FAC::R * W) * ESZ + 127) / 128 * 128;
+    // (tensor-map destinations 128-byte aligned, 128B-swizzled ones 1024)
+    static constexpr int BUF = ((MAP == MAP_STRIDED ? FAC::R * SW : FAC::R * W) * ESZ + 1023) / 1024 * 1024;
     static constexpr int SMEM = 2 * BUF + 16;
     // resident CTAs per SM the shared memory allows (registers are capped to match)
     static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024);
@@ -286,6 +292,12 @@ __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorM
                 tma_load_1d(buf + j * SW, row, sh ? sz1 : sz0, bar);
             }
         }
+    } else if (a.swz) {
+        if (lane == 0) {
+            constexpr int TR = R * W * (int)sizeof(V) / 128;  // 128-byte rows per tile
+            mbar_expect_tx(bar, (unsigned)(R * W * sizeof(V)));
+            tma_load_3d(buf, map, 0, 0, (int)(tile * (TR / a.swz_b1)), bar);
+        }
     } else if (lane == 0) {
         const long long n = (long long)g.nvalid * R;
         unsigned bytes = (unsigned)(n * sizeof(V));
@@ -337,7 +349,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
     // fp32 strided tiles (per-row shifted layout) keep register stores.
     constexpr bool TSTORE = !SHIFT;
     constexpr int NGL = FA::G(NS - 1) / GMIN;  // last-step groups per thread
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     V* const bufs = reinterpret_cast<V*>(smem_raw);
     unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem_raw + 2 * Pol::BUF);
 
@@ -392,7 +404,16 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
         // shared element of tile row `row` for this thread's column
         const int codd = SHIFT && !a.use_tmap ? (a.C & 1) : 0;
         const int b0 = SHIFT && !a.use_tmap ? (int)(geo.base & 1) : 0;
-        auto sref = [&](int row) -> V& { return scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)]; };
+        const int swx = a.swz;  // 0/1
+        auto sref = [&](int row) -> V& {
+            if constexpr (!STRIDED && (RADIX == 2 || RADIX == 4 || RADIX == 8)) {
+                const int e = c * R + row;
+                const int sw = sizeof(V) == 16 ? ((e >> 3) & 7) : (((e >> 4) & 7) << 1);
+                return buf[e ^ (sw & -swx)];
+            } else {
+                return scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)];
+            }
+        };
         V* __restrict__ gdst = a.dst + geo.base + (STRIDED ? c : (long long)c * R);
         // external twiddle base/step for this column: w_K0^{jj kf}, w_K0^{jj S}
         auto ext_pair = [&](int kf, int S, V& tw, V& st) {
@@ -569,6 +590,9 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                     if constexpr (STRIDED) {
                         const long long p = tile / a.tiles_per_panel;
                         tma_store_3d(&tmap_dst, buf, (int)(2 * first), 0, (int)(p * (R / a.rb)));
+                    } else if (a.swz) {
+                        constexpr int TR = R * W * (int)sizeof(V) / 128;
+                        tma_store_3d(&tmap_dst, buf, 0, 0, (int)(tile * (TR / a.swz_b1)));
                     } else {
                         const long long n = (long long)geo.nvalid * R;
                         unsigned bytes = (unsigned)(n * sizeof(V));
