@@ -477,7 +477,15 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     a.panel_elems = (long long)d.R * d.C;
     a.C = (int)d.C;
     a.tiles_per_panel = d.contig ? 1 : (int)((d.C + d.W - 1) / d.W);
-    a.tiles = d.contig ? (a.panels + d.W - 1) / d.W : a.panels * a.tiles_per_panel;
+    a.nsig = (long long)batch;
+    a.bps = per_signal;
+    if (((long long)p->total * (long long)p->esize) % 16 != 0) {
+        // fp32 signals of odd length: per-signal tile starts would break the
+        // bulk copies' 16-byte alignment; walk the batch as one run instead
+        a.nsig = 1;
+        a.bps = a.panels;
+    }
+    a.tiles = d.contig ? a.nsig * ((a.bps + d.W - 1) / d.W) : a.panels * a.tiles_per_panel;
     a.ext = d.ext;
     a.sq = (unsigned)d.sq;
     a.ext_bits = d.ext_bits;
@@ -495,7 +503,9 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     memset(&map_dst, 0, sizeof map_dst);
     a.use_tmap = d.use_tmap;
     a.rb = d.rb;
-    a.swz = d.swz && (a.panels % d.W == 0);
+    // swizzled staging needs every tile start on a box-row group boundary
+    a.swz = d.swz && (per_signal % d.W == 0) &&
+            (((long long)p->total * (long long)p->esize / 128) % d.swz_b1 == 0);
     a.swz_b1 = d.swz_b1;
     if (d.use_tmap) {
         ST_TRY(tensor_map(p, d, src, batch, &map));

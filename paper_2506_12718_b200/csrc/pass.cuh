@@ -45,6 +45,11 @@ template <typename T> struct PassArgs {
     const cplx<T>* src;
     cplx<T>* dst;
     long long tiles;
+    // CONTIG tiles are ordered block-major across the batch: tile t covers
+    // signal t % nsig, blocks [(t / nsig) W, +W) of it, so concurrently running
+    // CTAs share the filter block (reused from L2 across the batch)
+    long long nsig;
+    long long bps;           // blocks (panels) per signal
     long long panels;        // total panels over the batch
     long long panel_elems;   // R * C
     int C;                   // columns per panel (contiguous)
@@ -134,8 +139,13 @@ template <typename T, typename FAC, int MAP> struct TilePolicy {
         }
         int w = MAXW;
         while (w > 1 && FAC::GMIN * w > 512) --w;
-        if (MAP == MAP_CONTIG)
+        if (MAP == MAP_CONTIG) {
             while (w > 1 && FAC::GMIN * w > 256) --w;
+            // ~36 KB tiles: three double-buffered CTAs per SM
+            while (w > 1 && FAC::NS > 1 && FAC::R * w * ESZ > 36 * 1024) --w;
+            // keep tile bytes a multiple of 1 KB where possible (swizzled staging)
+            while (w > 1 && (FAC::R * w * ESZ) % 1024 != 0 && (FAC::R * (w - 1) * ESZ) % 1024 == 0) --w;
+        }
         while (w > 1 && FAC::R * rowslots(w) * ESZ > SMEM_BUDGET) --w;
         // at least one full warp: warp 0 issues the bulk copies
         while (FAC::GMIN * w < 32 && FAC::R * rowslots(w + 1) * ESZ <= SMEM_BUDGET) ++w;
@@ -213,9 +223,10 @@ template <int R, int W, bool STRIDED, typename T>
 __device__ __forceinline__ TileGeo tile_geo(const PassArgs<T>& a, long long tile) {
     TileGeo g;
     if (!STRIDED) {
-        g.first = tile * W;
-        const long long left = a.panels - g.first;
+        const long long sig = tile % a.nsig, tb = tile / a.nsig;
+        const long long left = a.bps - tb * W;
         g.nvalid = left < W ? (int)left : W;
+        g.first = sig * a.bps + tb * W;
         g.base = g.first * (long long)R;
     } else {
         const long long p = tile / a.tiles_per_panel;
@@ -294,9 +305,8 @@ __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorM
         }
     } else if (a.swz) {
         if (lane == 0) {
-            constexpr int TR = R * W * (int)sizeof(V) / 128;  // 128-byte rows per tile
             mbar_expect_tx(bar, (unsigned)(R * W * sizeof(V)));
-            tma_load_3d(buf, map, 0, 0, (int)(tile * (TR / a.swz_b1)), bar);
+            tma_load_3d(buf, map, 0, 0, (int)(g.base * (long long)sizeof(V) / 128 / a.swz_b1), bar);
         }
     } else if (lane == 0) {
         const long long n = (long long)g.nvalid * R;
@@ -591,8 +601,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                         const long long p = tile / a.tiles_per_panel;
                         tma_store_3d(&tmap_dst, buf, (int)(2 * first), 0, (int)(p * (R / a.rb)));
                     } else if (a.swz) {
-                        constexpr int TR = R * W * (int)sizeof(V) / 128;
-                        tma_store_3d(&tmap_dst, buf, 0, 0, (int)(tile * (TR / a.swz_b1)));
+                        tma_store_3d(&tmap_dst, buf, 0, 0, (int)(geo.base * (long long)sizeof(V) / 128 / a.swz_b1));
                     } else {
                         const long long n = (long long)geo.nvalid * R;
                         unsigned bytes = (unsigned)(n * sizeof(V));
