@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--graph", type=int, default=-1,
+                    help="capture a step in a CUDA graph (default: on for multi-call steps, config 1)")
     return ap.parse_args()
 
 
@@ -296,6 +298,30 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # launch-bound multi-call steps (config 1: 100 batch-1 calls) replay a
+    # captured CUDA graph of the same calls instead of re-launching from Python
+    use_graph = args.graph if args.graph >= 0 else int(calls > 1)
+    graph_launches = 0
+    if use_graph:
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        l0 = pf.kernel_launch_count()
+        with torch.cuda.stream(cs):
+            sptr_saved = sptr
+            sptr = C.c_void_p(cs.cuda_stream)
+            with torch.cuda.graph(g, stream=cs):
+                step()
+            sptr = sptr_saved
+        graph_launches = pf.kernel_launch_count() - l0
+        stream.wait_stream(cs)
+        plain_step = step
+
+        def step():  # noqa: F811
+            g.replay()
+
+        step()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
@@ -314,7 +340,7 @@ def main():
     tw1 = time.time()
     if world > 1:
         dist.barrier()
-    launches = pf.kernel_launch_count() - launches0
+    launches = pf.kernel_launch_count() - launches0 + graph_launches * args.steps
     ms_max = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
     # keep the GPU busy (untimed) until the clock sampler has >= 1 s of samples
     t_soak = time.time()
@@ -408,6 +434,7 @@ def main():
             "config": {"workload": f"config{cfg.idx}: {cfg.note}", "radix": cfg.radix, "dims": cfg.dims,
                        "batch_per_gpu": per, "calls_per_step": calls, "global_batch": per * world,
                        "precision": cfg.precision, "parallelism": f"batch-sharded x{world}",
+                       "cuda_graph": bool(use_graph),
                        "l2": f"inputs {per * S / 2**30:.2f} GiB per GPU per step > 126 MB L2 (no flush needed)"
                        if per * S > 2 * 126e6 else "inputs smaller than 2x L2; out-of-place fresh buffer per call"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

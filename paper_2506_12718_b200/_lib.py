@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpafft_b200.so")
+LIB_PATH = os.environ.get("PAFFT_LIB") or os.path.join(HERE, "libpafft_b200.so")  # PAFFT_LIB: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "

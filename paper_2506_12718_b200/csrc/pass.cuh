@@ -36,6 +36,11 @@
 
 #include "codelets.cuh"
 
+// cap on resident CTAs per SM the register allocation is sized for
+#ifndef PAFFT_MAX_MINB
+#define PAFFT_MAX_MINB 4
+#endif
+
 namespace pafft_b200 {
 
 enum PassKind : int { KIND_DIF = 0, KIND_DIT_FWD = 1, KIND_DIT_CONJ = 2, KIND_CONV = 3 };
@@ -167,7 +172,7 @@ template <typename T, typename FAC, int MAP> struct TilePolicy {
     static constexpr int SMEM = 2 * BUF + 16;
     // resident CTAs per SM the shared memory allows (registers are capped to match)
     static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024);
-    static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > 4 ? 4 : MINB_SMEM);
+    static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > PAFFT_MAX_MINB ? PAFFT_MAX_MINB : MINB_SMEM);
 };
 
 template <typename T>
