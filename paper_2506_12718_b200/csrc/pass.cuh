@@ -148,8 +148,10 @@ template <typename T, typename FAC, int MAP> struct TilePolicy {
             while (w > 1 && FAC::GMIN * w > 256) --w;
             // ~36 KB tiles: three double-buffered CTAs per SM
             while (w > 1 && FAC::NS > 1 && FAC::R * w * ESZ > 36 * 1024) --w;
-            // keep tile bytes a multiple of 1 KB where possible (swizzled staging)
-            while (w > 1 && (FAC::R * w * ESZ) % 1024 != 0 && (FAC::R * (w - 1) * ESZ) % 1024 == 0) --w;
+            // power-of-two blocks: power-of-two W, so tiles divide the batch and
+            // stay 1 KB multiples (swizzled staging)
+            if ((FAC::R & (FAC::R - 1)) == 0)
+                while (w & (w - 1)) --w;
         }
         while (w > 1 && FAC::R * rowslots(w) * ESZ > SMEM_BUDGET) --w;
         // at least one full warp: warp 0 issues the bulk copies
