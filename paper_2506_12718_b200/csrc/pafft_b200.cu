@@ -282,6 +282,8 @@ void build_groups(pafft_plan_t p) {
         if (t == 0) continue;
         const int lim = (q == 0) ? std::max(max_mid, 1) : std::max(max_str, 1);
         const int forced_mid = env_int("PAFFT_MID_STAGES", 0);
+        int mid_pref = 1;
+        while (mid_pref + 1 <= max_mid && ipow(p->radix, mid_pref + 1) * (long long)p->esize <= 64 * 1024) ++mid_pref;
         if (q == 0 && forced_mid > 0 && forced_mid < t && forced_mid <= max_mid) {
             // tuning override: contiguous group of exactly forced_mid stages,
             // the rest split evenly into strided groups
@@ -294,16 +296,20 @@ void build_groups(pafft_plan_t p) {
                 a += s;
             }
             p->groups.push_back({q, a, forced_mid});
-        } else if (q == 0 && t > max_mid) {
-            // outer strided groups, then the contiguous group (gets the remainder)
-            const int npass = (t + std::min(max_mid, max_str) - 1) / std::min(max_mid, max_str);
+        } else if (q == 0 && t > mid_pref) {
+            // Contiguous (CONV) group: the largest block of <= 64 KB (measured on
+            // B200: 2^12 fp64 for config 1, 3^7 for config 2, 5^5 for config 5);
+            // the remaining stages split evenly into strided groups.
+            const int mid = mid_pref;
+            const int rest = t - mid;
+            const int npass = (rest + max_str - 1) / max_str;
             int a = 0;
             for (int i = 0; i < npass; ++i) {
-                // even split, remainder to the last (contiguous, CONV) groups
-                const int s = t / npass + (i >= npass - t % npass ? 1 : 0);
+                const int s = rest / npass + (i >= npass - rest % npass ? 1 : 0);
                 p->groups.push_back({q, a, s});
                 a += s;
             }
+            p->groups.push_back({q, a, mid});
         } else {
             const int npass = (t + lim - 1) / lim;
             int rem = t, a = 0;
