@@ -504,6 +504,8 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     a.scale = (T)scale;
     a.has_scale = scale != 1.0;
     if (a.tiles == 0) return PAFFT_OK;
+    if (a.tiles > 0x7fffffffll || a.nsig > 0x7fffffffll)
+        return fail(PAFFT_INVALID_ARGUMENT, "batch too large for one launch (%lld tiles); split the call", a.tiles);
     CUtensorMap map, map_dst;
     memset(&map, 0, sizeof map);
     memset(&map_dst, 0, sizeof map_dst);

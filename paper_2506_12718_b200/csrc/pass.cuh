@@ -228,19 +228,24 @@ struct TileGeo {
 
 template <int R, int W, bool STRIDED, typename T>
 __device__ __forceinline__ TileGeo tile_geo(const PassArgs<T>& a, long long tile) {
+    // tile, nsig, bps, tiles_per_panel, C all fit 32 bits (checked on the host):
+    // 32-bit divisions keep the per-tile bookkeeping cheap
+    const unsigned t32 = (unsigned)tile;
     TileGeo g;
     if (!STRIDED) {
-        const long long sig = tile % a.nsig, tb = tile / a.nsig;
-        const long long left = a.bps - tb * W;
+        const unsigned ns = (unsigned)a.nsig;
+        const unsigned tb = t32 / ns, sig = t32 - tb * ns;
+        const long long left = a.bps - (long long)tb * W;
         g.nvalid = left < W ? (int)left : W;
-        g.first = sig * a.bps + tb * W;
+        g.first = (long long)sig * a.bps + (long long)tb * W;
         g.base = g.first * (long long)R;
     } else {
-        const long long p = tile / a.tiles_per_panel;
-        g.first = (tile - p * a.tiles_per_panel) * (long long)W;
+        const unsigned tpp = (unsigned)a.tiles_per_panel;
+        const unsigned p = t32 / tpp;
+        g.first = (long long)(t32 - p * tpp) * W;
         const long long left = a.C - g.first;
         g.nvalid = left < W ? (int)left : W;
-        g.base = p * a.panel_elems + g.first;
+        g.base = (long long)p * a.panel_elems + g.first;
     }
     return g;
 }
@@ -283,7 +288,7 @@ __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorM
         // one 3-D box {SW columns, rb rows, R/rb row groups} = the whole tile,
         // landing densely as [row][SW] (out-of-range columns zero-filled)
         if (lane == 0) {
-            const long long p = tile / a.tiles_per_panel;
+            const unsigned p = (unsigned)tile / (unsigned)a.tiles_per_panel;
             mbar_expect_tx(bar, (unsigned)(R * SW * sizeof(V)));
             tma_load_3d(buf, map, (int)(2 * g.first), 0, (int)(p * (R / a.rb)), bar);
         }
@@ -605,7 +610,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                 if (lane == 0) {
                     fence_proxy_async();
                     if constexpr (STRIDED) {
-                        const long long p = tile / a.tiles_per_panel;
+                        const unsigned p = (unsigned)tile / (unsigned)a.tiles_per_panel;
                         tma_store_3d(&tmap_dst, buf, (int)(2 * first), 0, (int)(p * (R / a.rb)));
                     } else if (a.swz) {
                         tma_store_3d(&tmap_dst, buf, 0, 0, (int)(geo.base * (long long)sizeof(V) / 128 / a.swz_b1));
