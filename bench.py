@@ -377,6 +377,7 @@ def main():
     value = convs / (ms_max * 1e-3)
     conv_gbs = value / world * workload.bytes_per_conv(cfg, world) / 1e9
     flops = workload.flops_per_conv(cfg)
+    fp_peak = 34.08 if cfg.precision == "f64" else 72.06  # DFMA / FFMA TFLOP/s, measured
 
     # ---- e2e: host buffers through the C-ABI (pinned H2D + conv + D2H timed)
     e2e = None
@@ -411,8 +412,12 @@ def main():
             count = cpu_sample_count(c64, threads)
             run, kind, sample = cpu_comparator(c64, count, threads)
             secs = run()
+            # one core, pafft's own methodology (bench.cpp:52-59)
+            run1, _, _ = cpu_comparator(c64, 1, 1)
+            secs1 = run1()
             cpu = {"value": count / secs, "unit": "conv/s", "cores": threads, "kind": kind,
-                   "sample": sample + f"; {threads} threads, one timed batch of {count}"}
+                   "sample": sample + f"; {threads} threads, one timed batch of {count}",
+                   "value_1core": 1.0 / secs1}
         except Exception as e:  # report, never substitute
             cpu = {"value": None, "unit": "conv/s", "cores": cpu_threads(), "kind": "unavailable",
                    "sample": f"{type(e).__name__}: {e}"}
@@ -444,8 +449,10 @@ def main():
                          "signals_per_launch": chunk,
                          "peak_source": peak_src},
             "conv_roofline": {"bytes_per_conv": workload.bytes_per_conv(cfg, world), "achieved_gbs_per_gpu": conv_gbs,
-                              "frac_of_hbm": conv_gbs / peak, "flops_per_conv": flops,
-                              "achieved_tflops_per_gpu": value / world * flops / 1e12},
+                              "frac_of_hbm": conv_gbs / peak, "frac_of_hbm_datasheet_8tbs": conv_gbs / 8000.0,
+                              "flops_per_conv": flops, "achieved_tflops_per_gpu": value / world * flops / 1e12,
+                              # FP peaks measured by tools/probes/peaks.cu (profiles/r01_peaks_probe.log)
+                              "fp_peak_tflops": fp_peak, "frac_of_fp_peak": value / world * flops / 1e12 / fp_peak},
             "passes": [{**infos[i], "ms": pass_ms[i]} for i in range(npass)],
             "e2e": e2e,
             "gpu_launches": launches,

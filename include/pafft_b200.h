@@ -96,6 +96,19 @@ void* pafft_filter_device_ghat_scaled(pafft_filter_t filter);
 pafft_status pafft_filter_sync_scaled(pafft_filter_t filter, void* stream);
 /* An empty filter bound to `plan`, to receive a broadcast ghat. */
 pafft_status pafft_filter_create_empty(pafft_plan_t plan, pafft_filter_t* out);
+/* Multi-GPU filter distribution: broadcast the prepared
+ * filter of NCCL rank `root` into every other filter over NCCL (NVLink), once
+ * per filter -- no per-call collective.  filters[i] sit on distinct devices,
+ * all with the same plan key (the receivers from pafft_filter_create_empty);
+ * comms[i] is the ncclComm_t of filters[i]'s device.  One process per GPU:
+ * each rank passes its own filter (ndev = 1) and communicator.  comms == NULL:
+ * single-process call over ndev devices, the library creates and caches the
+ * communicator clique (ncclCommInitAll; rank i = filters[i]).  streams may be
+ * NULL (legacy stream).  Receivers rebuild their kernel copy locally.  NCCL is
+ * resolved at first use (libnccl.so.2; the process's own copy if loaded);
+ * PAFFT_NCCL_ERROR if absent. */
+pafft_status pafft_filter_broadcast(pafft_filter_t* filters, int ndev, int root, void* const* comms,
+                                    void* const* streams);
 /* PreparedFilter::key == plan.key() (convolution.cpp:46). */
 int pafft_filter_matches(pafft_filter_t filter, pafft_plan_t plan);
 

@@ -453,6 +453,18 @@ def filter_device_tensor(filter, scaled=False):
     return torch.as_tensor(_View(), device=f"cuda:{plan.device}")
 
 
+def broadcast_filter_nccl(filters, root=0, comms=None, streams=None):
+    """pafft_filter_broadcast: NCCL broadcast of filters[root]'s prepared
+    spectrum into the other filters (distinct devices, same plan key).
+    Single process: comms=None lets the library build the communicator clique.
+    One process per GPU: pass this rank's filter and its ncclComm_t handle."""
+    n = len(filters)
+    arr = (C.c_void_p * n)(*[f._h for f in filters])
+    cm = (C.c_void_p * n)(*comms) if comms is not None else None
+    ss = (C.c_void_p * n)(*[_stream_ptr(s) for s in streams]) if streams is not None else None
+    _check(lib.pafft_filter_broadcast(arr, n, int(root), cm, ss))
+
+
 def filter_sync_scaled(filter, stream=None):
     _check(lib.pafft_filter_sync_scaled(filter._h, _stream_ptr(stream)))
 

@@ -44,6 +44,7 @@ _SIGS = {
     "pafft_filter_device_ghat_scaled": ([_vp], _vp),
     "pafft_filter_sync_scaled": ([_vp, _vp], _st),
     "pafft_filter_create_empty": ([_vp, C.POINTER(_vp)], _st),
+    "pafft_filter_broadcast": ([C.POINTER(_vp), C.c_int, C.c_int, C.POINTER(_vp), C.POINTER(_vp)], _st),
     "pafft_filter_matches": ([_vp, _vp], C.c_int),
     "pafft_convolve_permfree": ([_vp, _vp, _vp, _sz, _vp], _st),
     "pafft_convolve_permfree_oop": ([_vp, _vp, _vp, _vp, _sz, _vp], _st),

@@ -9,6 +9,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -1146,6 +1148,117 @@ pafft_status pafft_prepare_filter_from_impulse_device(pafft_plan_t p, const void
     ST_TRY(pafft_filter_sync_scaled(f, stream));
     CUDA_TRY(cudaStreamSynchronize(st));
     *out = guard.release();
+    return PAFFT_OK;
+}
+
+// ------------------------------------------------- multi-GPU filter --
+// NCCL is resolved at first use with dlopen("libnccl.so.2"): inside a process
+// that already loaded NCCL (torch.distributed) the loader returns that copy,
+// so the library never brings a second NCCL into the process.
+namespace {
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitAll) comm_init_all = nullptr;
+    decltype(&ncclCommUserRank) comm_user_rank = nullptr;
+    decltype(&ncclBroadcast) broadcast = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+        if (!h) {
+            const char* e = dlerror();
+            a.why = std::string("cannot load NCCL: ") + (e ? e : "libnccl.so.2 not found");
+            return a;
+        }
+        a.get_unique_id = (decltype(a.get_unique_id))dlsym(h, "ncclGetUniqueId");
+        a.comm_init_all = (decltype(a.comm_init_all))dlsym(h, "ncclCommInitAll");
+        a.comm_user_rank = (decltype(a.comm_user_rank))dlsym(h, "ncclCommUserRank");
+        a.broadcast = (decltype(a.broadcast))dlsym(h, "ncclBroadcast");
+        a.group_start = (decltype(a.group_start))dlsym(h, "ncclGroupStart");
+        a.group_end = (decltype(a.group_end))dlsym(h, "ncclGroupEnd");
+        a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
+        a.ok = a.comm_init_all && a.comm_user_rank && a.broadcast && a.group_start && a.group_end && a.error_string;
+        if (!a.ok) a.why = "libnccl.so.2 lacks the collective entry points";
+        return a;
+    }();
+    return api;
+}
+
+#define NCCL_TRY(x)                                                                                   \
+    do {                                                                                              \
+        const ncclResult_t r_ = (x);                                                                  \
+        if (r_ != ncclSuccess) return fail(PAFFT_NCCL_ERROR, "%s: %s", #x, nccl().error_string(r_)); \
+    } while (0)
+
+// communicator cliques the library created for single-process broadcasts,
+// keyed by the device list (kept for the life of the process)
+std::mutex g_clique_mu;
+std::map<std::vector<int>, std::vector<ncclComm_t>> g_cliques;
+}  // namespace
+
+pafft_status pafft_filter_broadcast(pafft_filter_t* filters, int ndev, int root, void* const* comms,
+                                    void* const* streams) {
+    if (!filters || ndev < 1) return fail(PAFFT_INVALID_ARGUMENT, "need at least one filter");
+    for (int i = 0; i < ndev; ++i) {
+        if (!filters[i]) return fail(PAFFT_INVALID_ARGUMENT, "null filter %d", i);
+        const pafft_filter_s& a = *filters[i];
+        const pafft_filter_s& b = *filters[0];
+        bool same = a.radix == b.radix && a.rank == b.rank && a.prec == b.prec;
+        for (int q = 0; same && q < a.rank; ++q) same = a.dims[q] == b.dims[q];
+        if (!same) return fail(PAFFT_FILTER_PLAN_MISMATCH, "filter %d does not match filter 0's plan key", i);
+        for (int j = 0; j < i; ++j)
+            if (filters[j]->device == a.device)
+                return fail(PAFFT_INVALID_ARGUMENT, "filters %d and %d share device %d", j, i, a.device);
+    }
+    const NcclApi& api = nccl();
+    if (!api.ok) return fail(PAFFT_NCCL_ERROR, "%s", api.why.c_str());
+    std::vector<ncclComm_t> cs(ndev);
+    if (comms) {
+        for (int i = 0; i < ndev; ++i) cs[i] = (ncclComm_t)comms[i];
+    } else {
+        if (root < 0 || root >= ndev) return fail(PAFFT_INVALID_ARGUMENT, "root %d out of range", root);
+        std::vector<int> devs(ndev);
+        for (int i = 0; i < ndev; ++i) devs[i] = filters[i]->device;
+        std::lock_guard<std::mutex> lk(g_clique_mu);
+        auto it = g_cliques.find(devs);
+        if (it == g_cliques.end()) {
+            std::vector<ncclComm_t> fresh(ndev);
+            NCCL_TRY(api.comm_init_all(fresh.data(), ndev, devs.data()));
+            it = g_cliques.emplace(devs, fresh).first;
+        }
+        cs = it->second;
+    }
+    const size_t count = filters[0]->plan->total * 2;  // reals
+    const ncclDataType_t dt = filters[0]->prec == 0 ? ncclFloat64 : ncclFloat32;
+    std::vector<int> is_root(ndev);
+    for (int i = 0; i < ndev; ++i) {
+        int r = 0;
+        NCCL_TRY(api.comm_user_rank(cs[i], &r));
+        is_root[i] = r == root;
+    }
+    // the unscaled ghat travels; receivers rebuild their kernel copy locally
+    NCCL_TRY(api.group_start());
+    for (int i = 0; i < ndev; ++i) {
+        CUDA_TRY(cudaSetDevice(filters[i]->device));
+        void* buf = filters[i]->ghat->p;
+        const ncclResult_t r =
+            api.broadcast(buf, buf, count, dt, root, cs[i], streams ? (cudaStream_t)streams[i] : (cudaStream_t)0);
+        if (r != ncclSuccess) {
+            api.group_end();
+            return fail(PAFFT_NCCL_ERROR, "ncclBroadcast: %s", api.error_string(r));
+        }
+    }
+    NCCL_TRY(api.group_end());
+    for (int i = 0; i < ndev; ++i)
+        if (!is_root[i]) ST_TRY(pafft_filter_sync_scaled(filters[i], streams ? streams[i] : nullptr));
     return PAFFT_OK;
 }
 
