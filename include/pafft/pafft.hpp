@@ -163,6 +163,7 @@ private:
 struct PlanKey {
     Radix radix;
     std::vector<std::size_t> dims;
+    std::vector<Radix> radices = {};  // per-axis radices of a mixed plan (empty: all == radix)
     bool operator==(const PlanKey&) const = default;
 };
 
@@ -173,9 +174,38 @@ public:
         pafft_plan_t h = nullptr;
         detail::check(pafft_plan_create(radix_value(radix), shape_.dims().data(), static_cast<int>(shape_.rank()),
                                         precision, device, &h));
+        init(h, std::vector<Radix>(shape_.rank(), radix));
+        key_ = PlanKey{radix_, shape_.dims()};
+    }
+    // Extension: one radix per axis.
+    Plan(const std::vector<Radix>& radices, TensorShape shape, int precision = PAFFT_F64, int device = -1)
+        : radix_(radices.empty() ? Radix::r2 : radices[0]), shape_(std::move(shape)) {
+        if (radices.size() != shape_.rank()) throw Error("one radix per axis required");
+        std::vector<unsigned> rs;
+        for (Radix r : radices) rs.push_back(radix_value(r));
+        pafft_plan_t h = nullptr;
+        detail::check(pafft_plan_create_mixed(rs.data(), shape_.dims().data(), static_cast<int>(shape_.rank()),
+                                              precision, device, &h));
+        init(h, radices);
+        key_ = PlanKey{radix_, shape_.dims(), radices};
+    }
+    Radix radix() const { return radix_; }
+    Radix radix(std::size_t q) const { return radices_[q]; }
+    const TensorShape& shape() const { return shape_; }
+    std::size_t total() const { return shape_.total(); }
+    unsigned depth(std::size_t q) const { return depths_[q]; }
+    const TwiddleTable& twiddles(std::size_t q) const { return twiddles_[q]; }
+    std::span<const std::uint32_t> rev_map(std::size_t q) const { return rev_maps_[q]; }
+    const PlanKey& key() const { return key_; }
+    pafft_plan_t handle() const { return h_.get(); }
+    const std::shared_ptr<pafft_plan_s>& shared_handle() const { return h_; }
+
+private:
+    void init(pafft_plan_t h, const std::vector<Radix>& radices) {
         h_ = std::shared_ptr<pafft_plan_s>(h, [](pafft_plan_t p) { pafft_plan_destroy(p); });
-        const unsigned r = radix_value(radix);
+        radices_ = radices;
         for (std::size_t q = 0; q < shape_.rank(); ++q) {
+            const unsigned r = radix_value(radices[q]);
             const std::size_t n = shape_.dim(q);
             unsigned t = 0;
             for (std::size_t v = n; v > 1; v /= r) ++t;
@@ -189,20 +219,10 @@ public:
             }
             rev_maps_.push_back(std::move(rev));
         }
-        key_ = PlanKey{radix_, shape_.dims()};
     }
-    Radix radix() const { return radix_; }
-    const TensorShape& shape() const { return shape_; }
-    std::size_t total() const { return shape_.total(); }
-    unsigned depth(std::size_t q) const { return depths_[q]; }
-    const TwiddleTable& twiddles(std::size_t q) const { return twiddles_[q]; }
-    std::span<const std::uint32_t> rev_map(std::size_t q) const { return rev_maps_[q]; }
-    const PlanKey& key() const { return key_; }
-    pafft_plan_t handle() const { return h_.get(); }
-    const std::shared_ptr<pafft_plan_s>& shared_handle() const { return h_; }
 
-private:
     Radix radix_;
+    std::vector<Radix> radices_;
     TensorShape shape_;
     std::shared_ptr<pafft_plan_s> h_;
     std::vector<unsigned> depths_;
@@ -212,6 +232,7 @@ private:
 };
 
 inline Plan plan_create(Radix radix, const TensorShape& shape) { return Plan(radix, shape); }
+inline Plan plan_create(const std::vector<Radix>& radices, const TensorShape& shape) { return Plan(radices, shape); }
 
 inline ComplexBuffer buffer_from_tensor(std::span<const std::complex<double>> values, const TensorShape& shape) {
     const std::size_t total = shape.total();

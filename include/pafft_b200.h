@@ -57,6 +57,14 @@ void pafft_last_error_dim(size_t* dim, size_t* extent);
  * `device` (-1 = current device). */
 pafft_status pafft_plan_create(unsigned radix, const size_t* dims, int rank, int precision, int device,
                                pafft_plan_t* out);
+/* Per-axis radices: axis q is a
+ * power of radices[q] and runs its own radix-radices[q] ladders; the prepared
+ * filter is the per-axis digit reversal (P_{r_d,n_d} (x) ... (x) P_{r_1,n_1}) g.
+ * pafft_plan_create(r, ...) == pafft_plan_create_mixed({r, r, ...}, ...). */
+pafft_status pafft_plan_create_mixed(const unsigned* radices, const size_t* dims, int rank, int precision,
+                                     int device, pafft_plan_t* out);
+/* radices: rank entries. */
+pafft_status pafft_plan_radices(pafft_plan_t plan, unsigned* radices);
 pafft_status pafft_plan_destroy(pafft_plan_t plan);
 /* Plan::radix/shape/total/depth (core.hpp:104-112). dims/depths: rank entries. */
 pafft_status pafft_plan_info(pafft_plan_t plan, unsigned* radix, int* rank, size_t* dims, unsigned* depths,

@@ -62,7 +62,8 @@ def _dims(dims):
 
 class _OrcPlan(C.Structure):
     _fields_ = [("radix", C.c_uint), ("rank", C.c_int), ("dims", _sz * 8), ("depth", C.c_uint * 8),
-                ("total", _sz), ("tw_re", _dp * 8), ("tw_im", _dp * 8), ("rev", C.POINTER(C.c_uint32) * 8)]
+                ("total", _sz), ("tw_re", _dp * 8), ("tw_im", _dp * 8), ("rev", C.POINTER(C.c_uint32) * 8),
+                ("radices", C.c_uint * 8)]
 
 
 class Oracle:
@@ -74,6 +75,8 @@ class Oracle:
         L = C.CDLL(path)
         self.L = L
         L.orc_plan_create.argtypes = [C.c_uint, C.POINTER(_sz), C.c_int, C.POINTER(C.POINTER(_OrcPlan))]
+        L.orc_plan_create_mixed.argtypes = [C.POINTER(C.c_uint), C.POINTER(_sz), C.c_int,
+                                             C.POINTER(C.POINTER(_OrcPlan))]
         L.orc_plan_destroy.argtypes = [C.POINTER(_OrcPlan)]
         for name in ("orc_permute_tensor", "orc_convolve_permfree_batch"):
             pass
@@ -147,7 +150,13 @@ class OraclePlan:
         self.total = int(np.prod(self.dims)) if self.dims else 0
         d, rank = _dims(self.dims)
         ptr = C.POINTER(_OrcPlan)()
-        st = self.L.orc_plan_create(radix, d, rank, C.byref(ptr))
+        if isinstance(radix, (list, tuple)):  # per-axis radices
+            rs = (C.c_uint * max(1, len(radix)))(*radix)
+            if len(radix) != rank:
+                raise OracleError(-1, f"{len(radix)} radices for {rank} dims")
+            st = self.L.orc_plan_create_mixed(rs, d, rank, C.byref(ptr))
+        else:
+            st = self.L.orc_plan_create(radix, d, rank, C.byref(ptr))
         if st:
             raise OracleError(st, f"plan_create(r={radix}, dims={dims})")
         self.ptr = ptr

@@ -40,19 +40,32 @@ static int radix_supported(unsigned r) {
 
 /* Plan::Plan, core.cpp:93-127; TwiddleTable, core.cpp:84-91. */
 int orc_plan_create(unsigned radix, const size_t* dims, int rank, orc_plan** out) {
+    unsigned radices[ORC_MAX_RANK];
+    for (int q = 0; q < ORC_MAX_RANK; ++q) radices[q] = radix;
     *out = NULL;
-    if (!radix_supported(radix)) return ORC_INVALID_ARGUMENT;
+    if (rank > ORC_MAX_RANK) return ORC_INVALID_ARGUMENT;
+    return orc_plan_create_mixed(radices, dims, rank, out);
+}
+
+/* Per-axis radix r_q: axis q is
+ * its own radix-r_q ladder with its own digit reversal P_{r_q, n_q}; the
+ * tensor structure (butterfly.cpp:423-466 mode loop) is unchanged. */
+int orc_plan_create_mixed(const unsigned* radices, const size_t* dims, int rank, orc_plan** out) {
+    *out = NULL;
     if (rank <= 0) return ORC_EMPTY_SHAPE;
     if (rank > ORC_MAX_RANK) return ORC_INVALID_ARGUMENT;
     for (int q = 0; q < rank; ++q) {
-        if (!is_power_of(dims[q], radix)) return ORC_NOT_A_POWER_OF_RADIX;
+        if (!radix_supported(radices[q])) return ORC_INVALID_ARGUMENT;
+        if (!is_power_of(dims[q], radices[q])) return ORC_NOT_A_POWER_OF_RADIX;
         if (dims[q] > 0xffffffffull) return ORC_INVALID_ARGUMENT;
     }
     orc_plan* p = (orc_plan*)calloc(1, sizeof(orc_plan));
-    p->radix = radix;
+    p->radix = radices[0];
     p->rank = rank;
     p->total = 1;
     for (int q = 0; q < rank; ++q) {
+        const unsigned radix = radices[q];
+        p->radices[q] = radix;
         const size_t n = dims[q];
         p->dims[q] = n;
         p->total *= n;
@@ -237,7 +250,7 @@ int orc_butterfly_line(const orc_plan* p, size_t dim, int variant, double* re, d
     if ((int)dim >= p->rank) return ORC_INVALID_ARGUMENT;
     if (len != p->dims[dim]) return ORC_SHAPE_MISMATCH;
     if (len == 1) return ORC_OK;
-    ladder(p->radix, variant, re, im, len, p->tw_re[dim], p->tw_im[dim]);
+    ladder(p->radices[dim], variant, re, im, len, p->tw_re[dim], p->tw_im[dim]);
     return ORC_OK;
 }
 
@@ -254,14 +267,14 @@ int orc_butterfly_tensor(const orc_plan* p, int variant, double* xr, double* xi)
         if (nq > 1) {
             if (stride == 1) {
                 for (size_t base = 0; base < p->total; base += nq)
-                    ladder(p->radix, variant, xr + base, xi + base, nq, p->tw_re[q], p->tw_im[q]);
+                    ladder(p->radices[q], variant, xr + base, xi + base, nq, p->tw_re[q], p->tw_im[q]);
             } else {
                 const size_t block = stride * nq;
                 for (size_t base = 0; base < p->total; base += block) {
                     for (size_t inner = 0; inner < stride; ++inner) {
                         const size_t start = base + inner;
                         for (size_t m = 0; m < nq; ++m) { sr[m] = xr[start + m * stride]; si[m] = xi[start + m * stride]; }
-                        ladder(p->radix, variant, sr, si, nq, p->tw_re[q], p->tw_im[q]);
+                        ladder(p->radices[q], variant, sr, si, nq, p->tw_re[q], p->tw_im[q]);
                         for (size_t m = 0; m < nq; ++m) { xr[start + m * stride] = sr[m]; xi[start + m * stride] = si[m]; }
                     }
                 }

@@ -57,9 +57,12 @@ typedef struct {
     double* tw_re[ORC_MAX_RANK];
     double* tw_im[ORC_MAX_RANK];
     uint32_t* rev[ORC_MAX_RANK];
+    unsigned radices[ORC_MAX_RANK]; /* per-axis radix (all equal to radix for pafft plans) */
 } orc_plan;
 
 int orc_plan_create(unsigned radix, const size_t* dims, int rank, orc_plan** out);
+/* Mixed per-axis radices: n_q = radices[q]^t_q. */
+int orc_plan_create_mixed(const unsigned* radices, const size_t* dims, int rank, orc_plan** out);
 void orc_plan_destroy(orc_plan* p);
 
 /* digit_reverse (permutation.cpp:27-37). Returns ORC_INDEX_OUT_OF_RANGE for j >= r^t. */

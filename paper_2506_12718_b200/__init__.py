@@ -105,15 +105,25 @@ class Plan:
     """Plan(radix, dims[, precision, device]) -- module.cpp:76-85.
 
     ``dims`` follow the numpy axis order of the arrays passed in (numpy axis q
-    is pafft dim q, module.cpp:30-35)."""
+    is pafft dim q, module.cpp:30-35).  ``radix`` may also be a sequence with
+    one radix per axis (mixed per-axis plans)."""
 
     def __init__(self, radix, dims, precision=F64, device=-1):
         dims = [int(d) for d in dims]
         arr = (C.c_size_t * max(len(dims), 1))(*dims)
         h = C.c_void_p()
-        _check(lib.pafft_plan_create(int(radix), arr, len(dims), int(precision), int(device), C.byref(h)))
+        if isinstance(radix, (list, tuple)):
+            if len(radix) != len(dims):
+                raise Error(f"{len(radix)} radices for {len(dims)} dimensions")
+            rs = (C.c_uint * max(len(radix), 1))(*[int(r) for r in radix])
+            _check(lib.pafft_plan_create_mixed(rs, arr, len(dims), int(precision), int(device), C.byref(h)))
+            self._radices = [int(r) for r in radix]
+            radix = self._radices[0] if len(set(self._radices)) == 1 else list(self._radices)
+        else:
+            _check(lib.pafft_plan_create(int(radix), arr, len(dims), int(precision), int(device), C.byref(h)))
+            self._radices = [int(radix)] * len(dims)
         self._h = h
-        self._radix = int(radix)
+        self._radix = radix if isinstance(radix, list) else int(radix)
         self._dims = dims
         self._precision = int(precision)
         dev = C.c_int()
@@ -129,6 +139,11 @@ class Plan:
     @property
     def radix(self):
         return self._radix
+
+    @property
+    def radices(self):
+        """Per-axis radices (all equal for a pafft Radix plan)."""
+        return list(self._radices)
 
     @property
     def dims(self):
@@ -148,7 +163,7 @@ class Plan:
 
     @property
     def depths(self):
-        return [round(math.log(d, self._radix)) if d > 1 else 0 for d in self._dims]
+        return [round(math.log(d, r)) if d > 1 else 0 for d, r in zip(self._dims, self._radices)]
 
     def describe(self):
         buf = C.create_string_buffer(8192)
@@ -161,7 +176,7 @@ class Plan:
         return n.value
 
     def key(self):
-        return (self._radix, tuple(self._dims), self._precision, self._device)
+        return (tuple(self._radices), tuple(self._dims), self._precision, self._device)
 
 
 class PreparedFilter:

@@ -29,6 +29,9 @@ _SIGS = {
     "pafft_last_error_dim": ([C.POINTER(_sz), C.POINTER(_sz)], None),
     "pafft_build_info": ([], C.c_char_p),
     "pafft_plan_create": ([C.c_uint, C.POINTER(_sz), C.c_int, C.c_int, C.c_int, C.POINTER(_vp)], _st),
+    "pafft_plan_create_mixed": ([C.POINTER(C.c_uint), C.POINTER(_sz), C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
+                                _st),
+    "pafft_plan_radices": ([_vp, C.POINTER(C.c_uint)], _st),
     "pafft_plan_destroy": ([_vp], _st),
     "pafft_plan_info": ([_vp, C.POINTER(C.c_uint), C.POINTER(C.c_int), C.POINTER(_sz), C.POINTER(C.c_uint),
                          C.POINTER(_sz), C.POINTER(C.c_int), C.POINTER(C.c_int)], _st),

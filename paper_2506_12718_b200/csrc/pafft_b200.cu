@@ -144,7 +144,8 @@ struct Group {
 }  // namespace
 
 struct pafft_plan_s {
-    unsigned radix = 0;
+    unsigned radix = 0;          // radix of axis 0 (the pafft Radix when uniform)
+    unsigned radices[8] = {0};   // per-axis radix
     int rank = 0;
     size_t dims[8] = {0};
     unsigned depth[8] = {0};
@@ -171,8 +172,9 @@ struct pafft_plan_s {
 };
 
 struct pafft_filter_s {
-    pafft_plan_t plan = nullptr;  // key: (radix, dims, precision, device)
+    pafft_plan_t plan = nullptr;  // key: (radices, dims, precision, device)
     unsigned radix = 0;
+    unsigned radices[8] = {0};
     int rank = 0;
     size_t dims[8] = {0};
     int prec = 0, device = 0;
@@ -273,19 +275,20 @@ int env_int(const char* name, int dflt) {
 // transposes).  Strided axes first (any order is valid: modes commute,
 // SPEC.md:226), then axis 0 split so its last group is a contiguous block.
 void build_groups(pafft_plan_t p) {
-    const int maxs = max_stages_compiled(p->prec, (int)p->radix, KIND_CONV, MAP_CONTIG);
-    const int max_mid = std::min(maxs, env_int("PAFFT_MAX_MID_STAGES", maxs));
-    int max_str = max_stages_compiled(p->prec, (int)p->radix, KIND_DIF, MAP_STRIDED);
-    if (p->radix == 2) max_str = std::min(max_str, 11);
-    max_str = std::min(max_str, env_int("PAFFT_MAX_STRIDED_STAGES", max_str));
     p->groups.clear();
     for (int q = p->rank - 1; q >= 0; --q) {
         const int t = (int)p->depth[q];
         if (t == 0) continue;
+        const unsigned radix = p->radices[q];
+        const int maxs = max_stages_compiled(p->prec, (int)radix, KIND_CONV, MAP_CONTIG);
+        const int max_mid = std::min(maxs, env_int("PAFFT_MAX_MID_STAGES", maxs));
+        int max_str = max_stages_compiled(p->prec, (int)radix, KIND_DIF, MAP_STRIDED);
+        if (radix == 2) max_str = std::min(max_str, 11);
+        max_str = std::min(max_str, env_int("PAFFT_MAX_STRIDED_STAGES", max_str));
         const int lim = (q == 0) ? std::max(max_mid, 1) : std::max(max_str, 1);
         const int forced_mid = env_int("PAFFT_MID_STAGES", 0);
         int mid_pref = 1;
-        while (mid_pref + 1 <= max_mid && ipow(p->radix, mid_pref + 1) * (long long)p->esize <= 64 * 1024) ++mid_pref;
+        while (mid_pref + 1 <= max_mid && ipow(radix, mid_pref + 1) * (long long)p->esize <= 64 * 1024) ++mid_pref;
         if (q == 0 && forced_mid > 0 && forced_mid < t && forced_mid <= max_mid) {
             // tuning override: contiguous group of exactly forced_mid stages,
             // the rest split evenly into strided groups
@@ -336,15 +339,16 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     d.axis = g.axis;
     d.a = g.a;
     d.s = g.s;
-    d.R = (int)ipow(p->radix, g.s);
-    d.K0 = n / ipow(p->radix, g.a);
+    const unsigned radix = p->radices[g.axis];
+    d.R = (int)ipow(radix, g.s);
+    d.K0 = n / ipow(radix, g.a);
     d.L = d.K0 / d.R;
     d.sq = sq;
     d.C = d.L * sq;
     d.contig = d.C == 1;
-    const KernelEntry* ke = find_kernel(p->prec, (int)p->radix, d.R, kind, d.contig ? MAP_CONTIG : MAP_STRIDED);
+    const KernelEntry* ke = find_kernel(p->prec, (int)radix, d.R, kind, d.contig ? MAP_CONTIG : MAP_STRIDED);
     if (!ke)
-        return fail(PAFFT_INVALID_ARGUMENT, "no kernel for radix %u R=%d kind %d map %d", p->radix, d.R, kind,
+        return fail(PAFFT_INVALID_ARGUMENT, "no kernel for radix %u R=%d kind %d map %d", radix, d.R, kind,
                     d.contig);
     d.fn = ke->fn;
     d.F[0] = ke->F0;
@@ -365,7 +369,7 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
         if (occ < 1) return fail(PAFFT_CUDA_ERROR, "pass kernel R=%d cannot be resident (smem %zu)", d.R, d.smem);
         d.max_ctas = (long long)occ * sms;
     }
-    if (d.contig && (p->radix == 2 || p->radix == 4 || p->radix == 8) && env_int("PAFFT_NO_SWIZZLE", 0) == 0) {
+    if (d.contig && (radix == 2 || radix == 4 || radix == 8) && env_int("PAFFT_NO_SWIZZLE", 0) == 0) {
         const long long tile_bytes = (long long)d.R * d.W * (long long)p->esize;
         if (tile_bytes % 1024 == 0) {
             const long long tr = tile_bytes / 128;
@@ -800,6 +804,8 @@ pafft_status set_device(pafft_plan_t p) {
 bool key_match(pafft_filter_t f, pafft_plan_t p) {
     if (f->radix != p->radix || f->rank != p->rank || f->prec != p->prec || f->device != p->device) return false;
     for (int q = 0; q < p->rank; ++q)
+        if (f->radices[q] != p->radices[q]) return false;
+    for (int q = 0; q < p->rank; ++q)
         if (f->dims[q] != p->dims[q]) return false;
     return true;
 }
@@ -902,9 +908,25 @@ pafft_status pafft_plan_create(unsigned radix, const size_t* dims, int rank, int
         return fail(PAFFT_INVALID_ARGUMENT, "radix must be 2, 3, 4, 5, or 8 (got %u)", radix);
     if (rank <= 0) return fail(PAFFT_EMPTY_SHAPE, "shape has no dimensions");
     if (rank > 8) return fail(PAFFT_INVALID_ARGUMENT, "rank %d exceeds 8", rank);
+    unsigned radices[8];
+    for (int q = 0; q < 8; ++q) radices[q] = radix;
+    return pafft_plan_create_mixed(radices, dims, rank, precision, device, out);
+}
+
+pafft_status pafft_plan_create_mixed(const unsigned* radices, const size_t* dims, int rank, int precision,
+                                     int device, pafft_plan_t* out) {
+    if (!out) return fail(PAFFT_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    if (rank <= 0) return fail(PAFFT_EMPTY_SHAPE, "shape has no dimensions");
+    if (rank > 8) return fail(PAFFT_INVALID_ARGUMENT, "rank %d exceeds 8", rank);
+    if (!radices || !dims) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    for (int q = 0; q < rank; ++q)
+        if (!radix_ok(radices[q]))
+            return fail(PAFFT_INVALID_ARGUMENT, "radix must be 2, 3, 4, 5, or 8 (got %u on axis %d)", radices[q], q);
     if (precision != PAFFT_F64 && precision != PAFFT_F32)
         return fail(PAFFT_INVALID_ARGUMENT, "unknown precision %d", precision);
     for (int q = 0; q < rank; ++q) {
+        const unsigned radix = radices[q];
         size_t n = dims[q];
         bool pow = n != 0;
         while (pow && n % radix == 0) n /= radix;
@@ -925,7 +947,8 @@ pafft_status pafft_plan_create(unsigned radix, const size_t* dims, int rank, int
     if (device < 0) CUDA_TRY(cudaGetDevice(&device));
     CUDA_TRY(cudaSetDevice(device));
     auto p = std::make_unique<pafft_plan_s>();
-    p->radix = radix;
+    p->radix = radices[0];
+    for (int q = 0; q < rank; ++q) p->radices[q] = radices[q];
     p->rank = rank;
     p->prec = precision;
     p->device = device;
@@ -935,7 +958,7 @@ pafft_status pafft_plan_create(unsigned radix, const size_t* dims, int rank, int
         p->dims[q] = dims[q];
         p->total *= dims[q];
         unsigned t = 0;
-        for (size_t n = dims[q]; n > 1; n /= radix) ++t;
+        for (size_t n = dims[q]; n > 1; n /= radices[q]) ++t;
         p->depth[q] = t;
     }
     build_groups(p.get());
@@ -945,6 +968,7 @@ pafft_status pafft_plan_create(unsigned radix, const size_t* dims, int rank, int
     ST_TRY(passes_ladder(p.get(), KIND_DIT_FWD, p->dit_fwd));
     ST_TRY(passes_ladder(p.get(), KIND_DIT_CONJ, p->dit_conj));
     for (int q = 0; q < rank; ++q) {
+        const unsigned radix = radices[q];
         std::vector<uint32_t> rev(dims[q]);
         for (size_t j = 0; j < dims[q]; ++j) {
             size_t v = j, o = 0;
@@ -981,6 +1005,12 @@ pafft_status pafft_plan_destroy(pafft_plan_t plan) {
     for (auto& e : plan->join)
         if (e) cudaEventDestroy(e);
     delete plan;
+    return PAFFT_OK;
+}
+
+pafft_status pafft_plan_radices(pafft_plan_t p, unsigned* radices) {
+    if (!p || !radices) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    for (int q = 0; q < p->rank; ++q) radices[q] = p->radices[q];
     return PAFFT_OK;
 }
 
@@ -1028,6 +1058,7 @@ static pafft_status new_filter(pafft_plan_t p, pafft_filter_t* out) {
     auto f = std::make_unique<pafft_filter_s>();
     f->plan = p;
     f->radix = p->radix;
+    for (int q = 0; q < p->rank; ++q) f->radices[q] = p->radices[q];
     f->rank = p->rank;
     for (int q = 0; q < p->rank; ++q) f->dims[q] = p->dims[q];
     f->prec = p->prec;
@@ -1212,7 +1243,7 @@ pafft_status pafft_filter_broadcast(pafft_filter_t* filters, int ndev, int root,
         const pafft_filter_s& a = *filters[i];
         const pafft_filter_s& b = *filters[0];
         bool same = a.radix == b.radix && a.rank == b.rank && a.prec == b.prec;
-        for (int q = 0; same && q < a.rank; ++q) same = a.dims[q] == b.dims[q];
+        for (int q = 0; same && q < a.rank; ++q) same = a.dims[q] == b.dims[q] && a.radices[q] == b.radices[q];
         if (!same) return fail(PAFFT_FILTER_PLAN_MISMATCH, "filter %d does not match filter 0's plan key", i);
         for (int j = 0; j < i; ++j)
             if (filters[j]->device == a.device)

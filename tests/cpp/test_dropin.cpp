@@ -155,6 +155,30 @@ int main() {
         for (double& v : wrapped.im) v = -v;
         CHECK(max_diff(direct, wrapped) < 1e-12);
     }
+    // per-axis radices (extension): a delay along axis 0
+    // shifts cyclically; keys tell mixed and uniform plans apart
+    {
+        const Plan plan = plan_create(std::vector<Radix>{Radix::r3, Radix::r2}, TensorShape{27, 16});
+        CHECK(plan.radix(0) == Radix::r3 && plan.radix(1) == Radix::r2 && plan.depth(0) == 3 && plan.depth(1) == 4);
+        ComplexBuffer h(plan.total());
+        h.re[1] = 1.0;
+        const PreparedFilter filter = prepare_filter(filter_from_impulse(h, plan), plan);
+        const ComplexBuffer x = random_buffer(plan.total(), 91);
+        ComplexBuffer y = x;
+        convolve_permfree(y, filter, plan);
+        ComplexBuffer want(plan.total());
+        for (std::size_t i1 = 0; i1 < 16; ++i1)
+            for (std::size_t i0 = 0; i0 < 27; ++i0) {
+                want.re[(i0 + 1) % 27 + 27 * i1] = x.re[i0 + 27 * i1];
+                want.im[(i0 + 1) % 27 + 27 * i1] = x.im[i0 + 27 * i1];
+            }
+        CHECK(max_diff(y, want) < 1e-13);
+        const Plan p24 = plan_create(std::vector<Radix>{Radix::r2, Radix::r4}, TensorShape{16, 16});
+        const PreparedFilter f24 = prepare_filter(random_buffer(256, 92), p24);
+        ComplexBuffer z = random_buffer(256, 93);
+        CHECK_THROWS_AS(convolve_permfree(z, f24, plan_create(Radix::r2, TensorShape{16, 16})), FilterPlanMismatch);
+        CHECK_THROWS_AS(plan_create(std::vector<Radix>{Radix::r3, Radix::r2}, TensorShape{27, 27}), NotAPowerOfRadix);
+    }
     std::printf("dropin: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
 }

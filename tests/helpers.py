@@ -48,3 +48,9 @@ GRID_ODD = (
     + [(3, d) for d in ([27, 81], [9, 9, 27], [3, 243], [81, 3])]
     + [(5, d) for d in ([25, 125], [5, 25], [125, 5, 5])]
 )
+
+# Per-axis radices: axis q is a power of radices[q].
+GRID_MIXED = [
+    ([3, 2], [27, 64]), ([2, 3], [64, 81]), ([5, 4], [25, 64]), ([4, 5], [256, 25]), ([2, 3, 5], [8, 9, 25]),
+    ([8, 3], [64, 27]), ([4, 5, 3], [16, 5, 9]), ([3, 8], [243, 8]), ([5, 2], [125, 32]), ([2, 4], [32, 16]),
+]

@@ -65,6 +65,23 @@ def test_plan_validation_contract_without_gpu():
         pf.Plan(2, [24])
 
 
+def test_mixed_radix_validation_without_gpu():
+    """Per-axis radices: validated per axis before any
+    device work."""
+    import paper_2506_12718_b200 as pf
+    with pytest.raises(pf.NotAPowerOfRadix) as e:
+        pf.Plan([3, 2], [27, 27])
+    assert (e.value.dim, e.value.extent) == (1, 27)
+    with pytest.raises(pf.NotAPowerOfRadix):
+        pf.Plan([5, 4], [25, 8])
+    with pytest.raises(RuntimeError):
+        pf.Plan([3, 7], [27, 49])
+    with pytest.raises(RuntimeError):
+        pf.Plan([3, 2], [27])
+    with pytest.raises(pf.EmptyShape):
+        pf.Plan([], [])
+
+
 def test_no_cpu_fallback_without_device():
     """The product path fails loudly instead of computing on the CPU."""
     import torch

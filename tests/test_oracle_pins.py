@@ -240,3 +240,53 @@ def test_live_reference_agreement(orc, ref):
         assert rel_l2(go, gr) <= 1e-15
         assert rel_l2(po.convolve_permfree(x, po.prepare_filter(go)),
                       pr.convolve_permfree(x, pr.prepare_filter(gr))) <= 1e-15
+
+
+# ------------------------------------------------------ per-axis radices
+def _rev(j, r, n):
+    o = 0
+    while n > 1:
+        o, j, n = o * r + j % r, j // r, n // r
+    return o
+
+
+def test_mixed_radix_oracle_pins(orc):
+    """a different radix per axis.  Pinned by pafft's
+    radix-agnostic direct sum and naive DFT (oracle.cpp:50-123 restated), by
+    numpy, by the per-axis digit reversal of the prepared filter, and by the
+    uniform-radix plan when all radices agree."""
+    from helpers import GRID_MIXED
+    for radices, dims in GRID_MIXED:
+        n = int(np.prod(dims))
+        x, h = rand_c(n, 71 + n), rand_c(n, 72 + n)
+        p = orc.plan(radices, dims)
+        g = p.filter_from_impulse(h)
+        if n <= 4096:
+            assert max_diff(g, orc.naive_dft(h, dims)) <= transform_tolerance(n, np.abs(h).max()) * 2
+            direct = orc.naive_conv(x, h, dims)
+        else:
+            shp = dims[::-1]
+            direct = np.fft.ifftn(np.fft.fftn(x.reshape(shp)) * np.fft.fftn(h.reshape(shp))).reshape(-1)
+        gh = p.prepare_filter(g)
+        # ghat = (P_{r_d,n_d} (x) ... (x) P_{r_1,n_1}) g, vec order (first index fastest)
+        idx = np.arange(n)
+        src = np.zeros(n, dtype=np.int64)
+        w = 1
+        rem = idx.copy()
+        for r, nq in zip(radices, dims):
+            iq = rem % nq
+            rem //= nq
+            src += np.array([_rev(int(v), r, nq) for v in range(nq)])[iq] * w
+            w *= nq
+        assert np.array_equal(gh, g[src])
+        yp = p.convolve_permfree(x, gh)
+        ys = p.convolve_standard(x, g)
+        assert rel_l2(yp, direct) <= 1e-13 and rel_l2(ys, direct) <= 1e-13
+        assert max_diff(yp, direct) <= convolution_tolerance(n, np.abs(x).max(), np.abs(h).max()) or n > 4096
+    # all radices equal: identical to the uniform plan, bit for bit
+    x, h = rand_c(729, 1), rand_c(729, 2)
+    pm, pu = orc.plan([3, 3], [27, 27]), orc.plan(3, [27, 27])
+    assert np.array_equal(pm.convolve_permfree(x, pm.prepare_filter(pm.filter_from_impulse(h))),
+                          pu.convolve_permfree(x, pu.prepare_filter(pu.filter_from_impulse(h))))
+    with pytest.raises(RuntimeError):
+        orc.plan([3, 2], [27, 27])  # 27 is not a power of 2
