@@ -119,6 +119,25 @@ struct DevBuf {
     }
 };
 
+// Per-call scratch, stream-ordered (cudaMallocAsync / cudaFreeAsync on the
+// call's stream): Plan stays immutable, so calls on distinct buffers may run
+// concurrently from several threads and streams.
+struct AsyncBuf {
+    void* p = nullptr;
+    cudaStream_t st = nullptr;
+    ~AsyncBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+// Per-call stream for the synchronous host-buffer entry points.
+struct CallStream {
+    cudaStream_t s = nullptr;
+    ~CallStream() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
 struct PassDesc {
     int kind = 0;
     int axis = 0, a = 0, s = 0;
@@ -159,13 +178,12 @@ struct pafft_plan_s {
     std::map<std::string, std::vector<const void*>> int_tables;            // split -> step tables
     std::map<long long, unsigned> ext_bits;
     std::vector<uint32_t*> rev_dev;            // per-axis digit reversal maps (device)
-    // scratch for permutation / host pipelines
-    std::unique_ptr<DevBuf> scratch;
     std::unique_ptr<DevBuf> stage[3];
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
     cudaStream_t work[2] = {nullptr, nullptr};  // L2-chunk pipeline streams
     cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
     std::mutex mu;
+    std::mutex host_mu;  // serialises the host-buffer pipeline (plan-owned streams + staging)
     // pass schedules, built once at plan creation (immutable afterwards)
     std::vector<PassDesc> pf, dif, dit_fwd, dit_conj;
     std::map<std::string, CUtensorMap> tmaps;
@@ -783,6 +801,22 @@ pafft_status hadamard_dev(pafft_plan_t p, const void* x, const void* g, void* y,
                                                                  p->total, n);
     CUDA_TRY(cudaGetLastError());
     ++g_launches;
+    return PAFFT_OK;
+}
+
+pafft_status async_alloc(pafft_plan_t p, AsyncBuf& b, size_t bytes, cudaStream_t st) {
+    static std::once_flag once[64];
+    if (p->device >= 0 && p->device < 64)
+        std::call_once(once[p->device], [&] {
+            // keep freed blocks in the device pool (no OS round trip per call)
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, p->device) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        });
+    b.st = st;
+    CUDA_TRY(cudaMallocAsync(&b.p, bytes ? bytes : 16, st));
     return PAFFT_OK;
 }
 
@@ -1435,8 +1469,8 @@ static void deinterleave(const double* in, size_t n, double* re, double* im) {
 // All host<->device traffic of the split (drop-in) paths is ordered on the
 // plan's own stream; the non-blocking plan streams do not synchronise with the
 // legacy default stream, so a plain cudaMemcpy would race the kernels.
-static pafft_status upload_split(pafft_plan_t p, const double* re, const double* im, size_t n, void* dev) {
-    cudaStream_t st = p->streams[0];
+static pafft_status upload_split(pafft_plan_t p, const double* re, const double* im, size_t n, void* dev,
+                                 cudaStream_t st) {
     std::vector<double> h(2 * n);
     interleave(re, im, n, h.data());
     if (p->prec == 0) {
@@ -1449,8 +1483,8 @@ static pafft_status upload_split(pafft_plan_t p, const double* re, const double*
     CUDA_TRY(cudaStreamSynchronize(st));
     return PAFFT_OK;
 }
-static pafft_status download_split(pafft_plan_t p, const void* dev, size_t n, double* re, double* im) {
-    cudaStream_t st = p->streams[0];
+static pafft_status download_split(pafft_plan_t p, const void* dev, size_t n, double* re, double* im,
+                                   cudaStream_t st) {
     std::vector<double> h(2 * n);
     if (p->prec == 0) {
         CUDA_TRY(cudaMemcpyAsync(h.data(), dev, n * 16, cudaMemcpyDeviceToHost, st));
@@ -1474,10 +1508,12 @@ pafft_status pafft_convolve_permfree_split(pafft_plan_t p, pafft_filter_t f, dou
     const size_t n = p->total * batch;
     DevBuf x;
     CUDA_TRY(cudaMalloc(&x.p, n * p->esize));
-    ST_TRY(upload_split(p, re, im, n, x.p));
-    ST_TRY(pafft_convolve_permfree(p, f, x.p, batch, p->streams[0]));
-    CUDA_TRY(cudaStreamSynchronize(p->streams[0]));
-    return download_split(p, x.p, n, re, im);
+    CallStream cs;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking));
+    ST_TRY(upload_split(p, re, im, n, x.p, cs.s));
+    ST_TRY(pafft_convolve_permfree(p, f, x.p, batch, cs.s));
+    CUDA_TRY(cudaStreamSynchronize(cs.s));
+    return download_split(p, x.p, n, re, im, cs.s);
 }
 
 pafft_status pafft_convolve_permfree_host_oop(pafft_plan_t p, pafft_filter_t f, const void* x_host, void* y_host,
@@ -1486,6 +1522,9 @@ pafft_status pafft_convolve_permfree_host_oop(pafft_plan_t p, pafft_filter_t f, 
     if (!key_match(f, p)) return fail(PAFFT_FILTER_PLAN_MISMATCH, "prepared filter does not belong to this plan");
     if (batch == 0) return PAFFT_OK;
     ST_TRY(set_device(p));
+    // the pipeline's streams and staging buffers belong to the plan: one
+    // host-buffer call at a time per plan (each call is synchronous)
+    std::lock_guard<std::mutex> lk(p->host_mu);
     const size_t sig_bytes = p->total * p->esize;
     // chunks of ~64 MiB pipelined over three streams: H2D(i+1) || conv(i) || D2H(i-1)
     size_t chunk = std::max<size_t>(1, (size_t)(64ull << 20) / sig_bytes);
@@ -1518,9 +1557,10 @@ pafft_status pafft_permute(pafft_plan_t p, void* x, size_t batch, void* stream) 
     if (!p) return fail(PAFFT_INVALID_ARGUMENT, "null plan");
     ST_TRY(set_device(p));
     cudaStream_t st = (cudaStream_t)stream;
-    ST_TRY(ensure(p->scratch, p->total * batch * p->esize));
-    ST_TRY(permute_dev(p, x, p->scratch->p, batch, st));
-    CUDA_TRY(cudaMemcpyAsync(x, p->scratch->p, p->total * batch * p->esize, cudaMemcpyDeviceToDevice, st));
+    AsyncBuf scratch;
+    ST_TRY(async_alloc(p, scratch, p->total * batch * p->esize, st));
+    ST_TRY(permute_dev(p, x, scratch.p, batch, st));
+    CUDA_TRY(cudaMemcpyAsync(x, scratch.p, p->total * batch * p->esize, cudaMemcpyDeviceToDevice, st));
     return PAFFT_OK;
 }
 
@@ -1528,10 +1568,11 @@ static pafft_status ladder_op(pafft_plan_t p, int kind, bool permute_first, doub
                               void* x, size_t batch, cudaStream_t st) {
     const std::vector<PassDesc>& ps = kind == KIND_DIF ? p->dif : kind == KIND_DIT_FWD ? p->dit_fwd : p->dit_conj;
     if (permute_first) {
-        ST_TRY(ensure(p->scratch, p->total * batch * p->esize));
-        ST_TRY(permute_dev(p, x, p->scratch->p, batch, st));
+        AsyncBuf scratch;
+        ST_TRY(async_alloc(p, scratch, p->total * batch * p->esize, st));
+        ST_TRY(permute_dev(p, x, scratch.p, batch, st));
         if (ps.empty()) {
-            CUDA_TRY(cudaMemcpyAsync(x, p->scratch->p, p->total * batch * p->esize, cudaMemcpyDeviceToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(x, scratch.p, p->total * batch * p->esize, cudaMemcpyDeviceToDevice, st));
             if (scale != 1.0) {
                 const unsigned long long n = p->total * batch;
                 if (p->prec == 0)
@@ -1541,7 +1582,7 @@ static pafft_status ladder_op(pafft_plan_t p, int kind, bool permute_first, doub
             }
             return PAFFT_OK;
         }
-        return run_ladder(p, ps, p->scratch->p, x, batch, mul, scale, st);
+        return run_ladder(p, ps, scratch.p, x, batch, mul, scale, st);
     }
     if (ps.empty() && scale != 1.0) {
         const unsigned long long n = p->total * batch;
@@ -1598,11 +1639,13 @@ pafft_status pafft_convolve_standard_split(pafft_plan_t p, const double* g_re, c
     DevBuf g, x;
     CUDA_TRY(cudaMalloc(&g.p, n * p->esize));
     CUDA_TRY(cudaMalloc(&x.p, n * batch * p->esize));
-    ST_TRY(upload_split(p, g_re, g_im, n, g.p));
-    ST_TRY(upload_split(p, re, im, n * batch, x.p));
-    ST_TRY(pafft_convolve_standard(p, g.p, x.p, batch, p->streams[0]));
-    CUDA_TRY(cudaStreamSynchronize(p->streams[0]));
-    return download_split(p, x.p, n * batch, re, im);
+    CallStream cs;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking));
+    ST_TRY(upload_split(p, g_re, g_im, n, g.p, cs.s));
+    ST_TRY(upload_split(p, re, im, n * batch, x.p, cs.s));
+    ST_TRY(pafft_convolve_standard(p, g.p, x.p, batch, cs.s));
+    CUDA_TRY(cudaStreamSynchronize(cs.s));
+    return download_split(p, x.p, n * batch, re, im, cs.s);
 }
 
 pafft_status pafft_transform_split(pafft_plan_t p, int op, double* re, double* im, size_t batch) {
@@ -1612,8 +1655,10 @@ pafft_status pafft_transform_split(pafft_plan_t p, int op, double* re, double* i
     const size_t n = p->total * batch;
     DevBuf x;
     CUDA_TRY(cudaMalloc(&x.p, n * p->esize));
-    ST_TRY(upload_split(p, re, im, n, x.p));
-    cudaStream_t st = p->streams[0];
+    CallStream cs;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking));
+    cudaStream_t st = cs.s;
+    ST_TRY(upload_split(p, re, im, n, x.p, st));
     switch (op) {
         case 0: ST_TRY(pafft_fft_forward(p, x.p, batch, st)); break;
         case 1: ST_TRY(pafft_fft_backward(p, x.p, batch, st)); break;
@@ -1625,7 +1670,7 @@ pafft_status pafft_transform_split(pafft_plan_t p, int op, double* re, double* i
         default: return fail(PAFFT_INVALID_ARGUMENT, "unknown transform op %d", op);
     }
     CUDA_TRY(cudaStreamSynchronize(st));
-    return download_split(p, x.p, n, re, im);
+    return download_split(p, x.p, n, re, im, st);
 }
 
 pafft_status pafft_filter_from_impulse_split(pafft_plan_t p, const double* h_re, const double* h_im, double* g_re,
