@@ -91,6 +91,16 @@ pafft_status pafft_prepare_filter_device(pafft_plan_t plan, const void* g_dev, v
  * Equals prepare_filter(filter_from_impulse(h)) up to rounding. */
 pafft_status pafft_prepare_filter_from_impulse_device(pafft_plan_t plan, const void* h_dev, void* stream,
                                                       pafft_filter_t* out);
+/* Filter-spectrum cache across plans: as
+ * pafft_prepare_filter_from_impulse_device, but a spectrum already prepared
+ * for the same plan key (radices, dims, precision, device) from the same
+ * impulse bytes (128-bit device content hash) is shared instead of
+ * recomputed; *hit (may be NULL) says which.  Cached spectra are held weakly:
+ * they live while any filter handle uses them.  The returned handle is owned
+ * by the caller as usual (pafft_filter_destroy). */
+pafft_status pafft_prepare_filter_from_impulse_cached(pafft_plan_t plan, const void* h_dev, void* stream,
+                                                      pafft_filter_t* out, int* hit);
+void pafft_filter_cache_stats(uint64_t* hits, uint64_t* misses, uint64_t* live);
 pafft_status pafft_filter_destroy(pafft_filter_t filter);
 /* PreparedFilter::ghat readback (split, double). */
 pafft_status pafft_filter_ghat_split(pafft_filter_t filter, double* re, double* im);

@@ -182,6 +182,8 @@ class Plan:
 class PreparedFilter:
     """Filter spectrum digit-reversed once for reuse (convolution.hpp:9-12)."""
 
+    cache_hit = False
+
     def __init__(self, handle, plan):
         self._h = handle
         self._plan = plan  # keeps the plan (and its device tables) alive
@@ -438,13 +440,31 @@ def prepare_filter_device(g, plan, stream=None):
     return PreparedFilter(h, plan)
 
 
-def prepare_filter_from_impulse(h, plan, stream=None):
-    """ghat = A^T h directly on the device: zero permutation passes."""
+def prepare_filter_from_impulse(h, plan, stream=None, cache=False):
+    """ghat = A^T h directly on the device: zero permutation passes.
+
+    cache=True: reuse a spectrum already prepared from the same impulse bytes
+    for any plan with the same key (filter-spectrum cache across plans); the
+    returned filter's ``cache_hit`` says whether it was shared."""
     _dtype_ok(h, plan)
     out = C.c_void_p()
+    if cache:
+        hit = C.c_int()
+        _check(lib.pafft_prepare_filter_from_impulse_cached(plan._h, C.c_void_p(h.data_ptr()), _stream_ptr(stream),
+                                                             C.byref(out), C.byref(hit)))
+        f = PreparedFilter(out, plan)
+        f.cache_hit = bool(hit.value)
+        return f
     _check(lib.pafft_prepare_filter_from_impulse_device(plan._h, C.c_void_p(h.data_ptr()), _stream_ptr(stream),
                                                          C.byref(out)))
     return PreparedFilter(out, plan)
+
+
+def filter_cache_stats():
+    """(hits, misses, live entries) of the filter-spectrum cache."""
+    a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    lib.pafft_filter_cache_stats(C.byref(a), C.byref(b), C.byref(c))
+    return a.value, b.value, c.value
 
 
 def empty_filter(plan):

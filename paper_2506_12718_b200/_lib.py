@@ -41,6 +41,8 @@ _SIGS = {
     "pafft_prepare_filter_split": ([_vp, _dp, _dp, C.POINTER(_vp)], _st),
     "pafft_prepare_filter_device": ([_vp, _vp, _vp, C.POINTER(_vp)], _st),
     "pafft_prepare_filter_from_impulse_device": ([_vp, _vp, _vp, C.POINTER(_vp)], _st),
+    "pafft_prepare_filter_from_impulse_cached": ([_vp, _vp, _vp, C.POINTER(_vp), C.POINTER(C.c_int)], _st),
+    "pafft_filter_cache_stats": ([C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], None),
     "pafft_filter_destroy": ([_vp], _st),
     "pafft_filter_ghat_split": ([_vp, _dp, _dp], _st),
     "pafft_filter_device_ghat": ([_vp], _vp),

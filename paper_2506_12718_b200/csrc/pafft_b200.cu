@@ -22,6 +22,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/pafft_b200.h"
@@ -196,8 +197,8 @@ struct pafft_filter_s {
     int rank = 0;
     size_t dims[8] = {0};
     int prec = 0, device = 0;
-    std::unique_ptr<DevBuf> ghat;         // unscaled, plan precision
-    std::unique_ptr<DevBuf> ghat_scaled;  // x (1/N), plan precision
+    std::shared_ptr<DevBuf> ghat;         // unscaled, plan precision
+    std::shared_ptr<DevBuf> ghat_scaled;  // x (1/N), plan precision (shared by cached filters)
 };
 
 namespace {
@@ -1097,8 +1098,12 @@ static pafft_status new_filter(pafft_plan_t p, pafft_filter_t* out) {
     for (int q = 0; q < p->rank; ++q) f->dims[q] = p->dims[q];
     f->prec = p->prec;
     f->device = p->device;
-    ST_TRY(ensure(f->ghat, p->total * p->esize));
-    ST_TRY(ensure(f->ghat_scaled, p->total * p->esize));
+    for (std::shared_ptr<DevBuf>* b : {&f->ghat, &f->ghat_scaled}) {
+        auto nb = std::make_shared<DevBuf>();
+        CUDA_TRY(cudaMalloc(&nb->p, p->total * p->esize ? p->total * p->esize : 16));
+        nb->bytes = p->total * p->esize;
+        *b = std::move(nb);
+    }
     *out = f.release();
     return PAFFT_OK;
 }
@@ -1325,6 +1330,123 @@ pafft_status pafft_filter_broadcast(pafft_filter_t* filters, int ndev, int root,
     for (int i = 0; i < ndev; ++i)
         if (!is_root[i]) ST_TRY(pafft_filter_sync_scaled(filters[i], streams ? streams[i] : nullptr));
     return PAFFT_OK;
+}
+
+// ------------------------------------------ filter-spectrum cache --
+// Prepared spectra keyed by (plan key, 128-bit content hash of the impulse),
+// shared across plans with the same key.  Entries are
+// weak: a spectrum lives as long as some filter handle uses it.
+namespace {
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+// order-dependent sums of two independent word mixes (commutative reductions)
+__global__ void content_hash_kernel(const unsigned long long* __restrict__ w, unsigned long long n,
+                                    unsigned long long* out) {
+    unsigned long long h1 = 0, h2 = 0;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long v = w[i];
+        h1 += mix64(v + 0x9e3779b97f4a7c15ULL * (i + 1));
+        h2 += mix64((v ^ 0xd6e8feb86659fd93ULL) + 0xc2b2ae3d27d4eb4fULL * (i + 7)) | 1ull;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        h1 += __shfl_xor_sync(0xffffffffu, h1, o);
+        h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, h1);
+        atomicAdd(out + 1, h2);
+    }
+}
+
+struct CacheKey {
+    std::vector<unsigned> radices;
+    std::vector<size_t> dims;
+    int prec, device;
+    unsigned long long h1, h2;
+    bool operator<(const CacheKey& o) const {
+        return std::tie(radices, dims, prec, device, h1, h2) < std::tie(o.radices, o.dims, o.prec, o.device, o.h1, o.h2);
+    }
+};
+struct CacheEntry {
+    std::weak_ptr<DevBuf> ghat, ghat_scaled;
+};
+std::mutex g_cache_mu;
+std::map<CacheKey, CacheEntry> g_cache;
+std::atomic<unsigned long long> g_cache_hits{0}, g_cache_misses{0};
+}  // namespace
+
+pafft_status pafft_prepare_filter_from_impulse_cached(pafft_plan_t p, const void* h_dev, void* stream,
+                                                      pafft_filter_t* out, int* hit) {
+    if (!p || !out || !h_dev) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ST_TRY(set_device(p));
+    cudaStream_t st = (cudaStream_t)stream;
+    AsyncBuf hb;
+    ST_TRY(async_alloc(p, hb, 16, st));
+    CUDA_TRY(cudaMemsetAsync(hb.p, 0, 16, st));
+    const unsigned long long words = (unsigned long long)p->total * p->esize / 8;
+    content_hash_kernel<<<(unsigned)std::min<unsigned long long>((words + 255) / 256, 148ull * 8), 256, 0, st>>>(
+        (const unsigned long long*)h_dev, words, (unsigned long long*)hb.p);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long hh[2];
+    CUDA_TRY(cudaMemcpyAsync(hh, hb.p, 16, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CacheKey key{std::vector<unsigned>(p->radices, p->radices + p->rank), std::vector<size_t>(p->dims, p->dims + p->rank),
+                 p->prec, p->device, hh[0], hh[1]};
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto it = g_cache.find(key);
+        if (it != g_cache.end()) {
+            auto g = it->second.ghat.lock();
+            auto gs = it->second.ghat_scaled.lock();
+            if (g && gs) {
+                auto f = std::make_unique<pafft_filter_s>();
+                f->plan = p;
+                f->radix = p->radix;
+                f->rank = p->rank;
+                for (int q = 0; q < p->rank; ++q) {
+                    f->dims[q] = p->dims[q];
+                    f->radices[q] = p->radices[q];
+                }
+                f->prec = p->prec;
+                f->device = p->device;
+                f->ghat = std::move(g);
+                f->ghat_scaled = std::move(gs);
+                *out = f.release();
+                if (hit) *hit = 1;
+                ++g_cache_hits;
+                return PAFFT_OK;
+            }
+            g_cache.erase(it);
+        }
+    }
+    pafft_filter_t f = nullptr;
+    ST_TRY(pafft_prepare_filter_from_impulse_device(p, h_dev, stream, &f));
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        // drop expired entries, then publish this one
+        for (auto it = g_cache.begin(); it != g_cache.end();)
+            it = it->second.ghat.expired() ? g_cache.erase(it) : std::next(it);
+        g_cache[key] = CacheEntry{f->ghat, f->ghat_scaled};
+    }
+    ++g_cache_misses;
+    if (hit) *hit = 0;
+    *out = f;
+    return PAFFT_OK;
+}
+
+void pafft_filter_cache_stats(uint64_t* hits, uint64_t* misses, uint64_t* live) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    if (hits) *hits = g_cache_hits.load();
+    if (misses) *misses = g_cache_misses.load();
+    if (live) {
+        uint64_t n = 0;
+        for (auto& e : g_cache) n += e.second.ghat.expired() ? 0 : 1;
+        *live = n;
+    }
 }
 
 pafft_status pafft_filter_destroy(pafft_filter_t f) {

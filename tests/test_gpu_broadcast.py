@@ -78,3 +78,36 @@ def test_two_device_broadcast(pf, torch, orc):
     y1 = pf.convolve_permfree_out(torch.from_numpy(x).to("cuda:1"), torch.empty(p1.total, dtype=torch.complex128,
                                   device="cuda:1"), f1, p1).cpu()
     assert torch.equal(y0, y1)
+
+
+def test_filter_spectrum_cache_across_plans(pf, torch):
+    """a spectrum prepared from the same impulse for a
+    plan with the same key is shared, not recomputed; held weakly."""
+    import gc
+    p1, p2 = pf.Plan(3, [2187]), pf.Plan(3, [2187])
+    rng = np.random.default_rng(11)
+    h = torch.from_numpy(rng.standard_normal(2187) + 1j * rng.standard_normal(2187)).cuda()
+    h0, m0, _ = pf.filter_cache_stats()
+    f1 = pf.prepare_filter_from_impulse(h, p1, cache=True)
+    f2 = pf.prepare_filter_from_impulse(h, p2, cache=True)
+    assert not f1.cache_hit and f2.cache_hit
+    assert f1.device_ghat_ptr(True) == f2.device_ghat_ptr(True)
+    ref = pf.prepare_filter_from_impulse(h, p2)  # uncached: same bits
+    assert torch.equal(pf.filter_device_tensor(f2), pf.filter_device_tensor(ref))
+    x = torch.from_numpy(rng.uniform(-1, 1, (2, 2187)) + 0j).cuda()
+    y1 = pf.convolve_permfree_out(x, torch.empty_like(x), f1, p1)
+    y2 = pf.convolve_permfree_out(x, torch.empty_like(x), f2, p2)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    # other bytes, other key -> misses
+    g = h.clone()
+    g[5] += 1.0
+    assert not pf.prepare_filter_from_impulse(g, p1, cache=True).cache_hit
+    assert not pf.prepare_filter_from_impulse(h.to(torch.complex64), pf.Plan(3, [2187], precision=pf.F32),
+                                              cache=True).cache_hit
+    hits, misses, _ = pf.filter_cache_stats()
+    assert hits - h0 >= 1 and misses - m0 >= 3
+    # weak entries: once every handle is gone the spectrum is released
+    del f1, f2
+    gc.collect()
+    assert not pf.prepare_filter_from_impulse(h, p1, cache=True).cache_hit
