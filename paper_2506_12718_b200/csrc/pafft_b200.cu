@@ -499,6 +499,8 @@ pafft_status tensor_map_swz(pafft_plan_t p, const PassDesc& d, const void* src, 
 template <typename T>
 pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
                       const void* ghat, const void* mul, double scale, cudaStream_t st, long long grid_cap) {
+    if (((uintptr_t)src | (uintptr_t)dst) & 15u)
+        return fail(PAFFT_INVALID_ARGUMENT, "device buffers must be 16-byte aligned (TMA staging)");
     PassArgs<T> a;
     memset(&a, 0, sizeof a);
     a.src = (const cplx<T>*)src;
@@ -830,6 +832,16 @@ pafft_status ensure(std::unique_ptr<DevBuf>& b, size_t bytes) {
     b = std::move(nb);
     return PAFFT_OK;
 }
+
+// Pass kernels stage tiles with TMA, which needs 16-byte aligned global
+// addresses: fp64 element pointers always are; fp32 views may sit 8 bytes off.
+bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; }
+#define ALIGN_TRY(ptr)                                                                                       \
+    do {                                                                                                     \
+        if (!aligned16(ptr))                                                                                 \
+            return fail(PAFFT_INVALID_ARGUMENT, "device buffer %s=%p is not 16-byte aligned (TMA staging)", \
+                        #ptr, (const void*)(ptr));                                                           \
+    } while (0)
 
 pafft_status set_device(pafft_plan_t p) {
     CUDA_TRY(cudaSetDevice(p->device));
@@ -1209,6 +1221,7 @@ pafft_status pafft_prepare_filter_split(pafft_plan_t p, const double* g_re, cons
 pafft_status pafft_prepare_filter_from_impulse_device(pafft_plan_t p, const void* h_dev, void* stream,
                                                       pafft_filter_t* out) {
     if (!p || !out || !h_dev) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ALIGN_TRY(h_dev);
     ST_TRY(set_device(p));
     pafft_filter_t f;
     ST_TRY(new_filter(p, &f));
@@ -1382,6 +1395,7 @@ std::atomic<unsigned long long> g_cache_hits{0}, g_cache_misses{0};
 pafft_status pafft_prepare_filter_from_impulse_cached(pafft_plan_t p, const void* h_dev, void* stream,
                                                       pafft_filter_t* out, int* hit) {
     if (!p || !out || !h_dev) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ALIGN_TRY(h_dev);
     ST_TRY(set_device(p));
     cudaStream_t st = (cudaStream_t)stream;
     AsyncBuf hb;
@@ -1500,6 +1514,8 @@ pafft_status pafft_convolve_permfree_oop(pafft_plan_t p, pafft_filter_t f, const
     if (!key_match(f, p)) return fail(PAFFT_FILTER_PLAN_MISMATCH, "prepared filter does not belong to this plan");
     if (batch == 0) return PAFFT_OK;
     if (!x_dev || !y_dev) return fail(PAFFT_INVALID_ARGUMENT, "null buffer");
+    ALIGN_TRY(x_dev);
+    ALIGN_TRY(y_dev);
     ST_TRY(set_device(p));
     cudaStream_t st = (cudaStream_t)stream;
     const std::vector<PassDesc>& ps = p->pf;
@@ -1688,6 +1704,7 @@ pafft_status pafft_permute(pafft_plan_t p, void* x, size_t batch, void* stream) 
 
 static pafft_status ladder_op(pafft_plan_t p, int kind, bool permute_first, double scale, const void* mul,
                               void* x, size_t batch, cudaStream_t st) {
+    ALIGN_TRY(x);
     const std::vector<PassDesc>& ps = kind == KIND_DIF ? p->dif : kind == KIND_DIT_FWD ? p->dit_fwd : p->dit_conj;
     if (permute_first) {
         AsyncBuf scratch;
@@ -1740,6 +1757,7 @@ pafft_status pafft_fft_transposed(pafft_plan_t p, void* x, size_t batch, void* s
 
 pafft_status pafft_convolve_standard(pafft_plan_t p, const void* g_dev, void* x, size_t batch, void* stream) {
     if (!p || !g_dev) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ALIGN_TRY(x);
     ST_TRY(set_device(p));
     cudaStream_t st = (cudaStream_t)stream;
     // fft_forward (permute #1 + A), o g fused into A's last pass, fft_backward (permute #2 + A-bar + 1/N)

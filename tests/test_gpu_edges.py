@@ -1,0 +1,120 @@
+"""Edge cases and maximum sizes on the GPU: extent-1 axes, empty batches,
+device buffers the kernels cannot stage (fp32 pointers off a 16-byte
+boundary) and launch-size limits fail cleanly, and the largest practical
+plans (2^27, 3^17, 5^11 points, 8192^2, 512^3) pass size-independent
+properties on device: delta -> identity, shifted delta -> cyclic shift,
+linearity."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from helpers import rand_c, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pf():
+    import paper_2506_12718_b200 as pf
+    return pf
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.mark.parametrize("radix,dims", [(2, [1]), (3, [1, 27]), (2, [16, 1]), (5, [1, 1, 25]), (4, [1, 4, 1])],
+                         ids=lambda v: str(v))
+def test_extent_one_axes(pf, torch, orc, radix, dims):
+    n = int(np.prod(dims))
+    x, h = rand_c(n, 1), rand_c(n, 2)
+    plan = pf.Plan(radix, dims)
+    f = pf.prepare_filter_from_impulse(torch.from_numpy(h).cuda(), plan)
+    y = pf.convolve_permfree_out(torch.from_numpy(x).cuda(), torch.empty(n, dtype=torch.complex128, device="cuda"),
+                                 f, plan).cpu().numpy()
+    shp = dims[::-1]
+    want = np.fft.ifftn(np.fft.fftn(x.reshape(shp)) * np.fft.fftn(h.reshape(shp))).reshape(-1)
+    assert rel_l2(y, want) <= 1e-13
+    op = orc.plan(radix, dims)
+    assert rel_l2(y, op.convolve_permfree(x, op.prepare_filter(op.filter_from_impulse(h)))) <= 1e-13
+
+
+def test_empty_batch_is_a_no_op(pf, torch):
+    plan = pf.Plan(3, [243])
+    f = pf.prepare_filter_from_impulse(torch.from_numpy(rand_c(243, 1)).cuda(), plan)
+    x = torch.empty(0, 243, dtype=torch.complex128, device="cuda")
+    pf.convolve_permfree_(x, f, plan)
+    pf.convolve_permfree_out(x, torch.empty_like(x), f, plan)
+    torch.cuda.synchronize()
+
+
+def test_unstageable_buffers_fail_cleanly(pf, torch):
+    """fp32 device pointers 8 bytes off a 16-byte boundary cannot feed TMA:
+    a clean error, never a wrong answer."""
+    plan = pf.Plan(3, [2187], precision=pf.F32)
+    f = pf.prepare_filter_from_impulse(torch.from_numpy(rand_c(2187, 1)).to("cuda", torch.complex64), plan)
+    base = torch.from_numpy(rand_c(2 * 2187 + 1, 2)).to("cuda", torch.complex64)
+    x = base[1:2188]
+    assert x.data_ptr() % 16 == 8
+    with pytest.raises(RuntimeError):
+        pf.convolve_permfree_out(x, torch.empty(2187, dtype=torch.complex64, device="cuda"), f, plan)
+    # aligned views of the same storage work
+    xa = base[2:2189]
+    assert xa.data_ptr() % 16 == 0
+    y = pf.convolve_permfree_out(xa, torch.empty(2187, dtype=torch.complex64, device="cuda"), f, plan)
+    torch.cuda.synchronize()
+    assert torch.isfinite(torch.view_as_real(y)).all()
+
+
+def test_launch_size_limit_is_reported(pf):
+    """More than 2^31 tiles in one call: INVALID_ARGUMENT before any memory
+    is touched (the caller splits the batch)."""
+    from paper_2506_12718_b200 import _lib
+    plan = pf.Plan(2, [2])
+    f = pf.empty_filter(plan)
+    st = _lib.lib.pafft_convolve_permfree_oop(plan._h, f._h, C.c_void_p(0x10000), C.c_void_p(0x20000),
+                                              C.c_size_t(2 ** 31 + 5), None)
+    assert st == 7  # PAFFT_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("radix,dims", [(2, [1 << 27]), (3, [3 ** 17]), (5, [5 ** 11]), (2, [8192, 8192]),
+                                        (2, [512, 512, 512]), (3, [3 ** 8, 3 ** 7])],
+                         ids=lambda v: str(v))
+def test_maximum_sizes_properties(pf, torch, radix, dims):
+    n = int(np.prod(dims))
+    plan = pf.Plan(radix, dims)
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.complex(torch.rand(n, device="cuda", dtype=torch.float64, generator=g) * 2 - 1,
+                      torch.rand(n, device="cuda", dtype=torch.float64, generator=g) * 2 - 1)
+    # delta -> identity
+    d = torch.zeros(n, dtype=torch.complex128, device="cuda")
+    d[0] = 1
+    y = pf.convolve_permfree_out(x, torch.empty_like(x), pf.prepare_filter_from_impulse(d, plan), plan)
+    assert float(torch.linalg.vector_norm(y - x) / torch.linalg.vector_norm(x)) <= 1e-13
+    # shifted delta -> cyclic shift along axis 0 (and axis 1 for multi-dim)
+    s0 = 3
+    idx = s0 + (dims[0] * 2 if len(dims) > 1 else 0)
+    d.zero_()
+    d[idx] = 1
+    y = pf.convolve_permfree_out(x, y, pf.prepare_filter_from_impulse(d, plan), plan)
+    xs = x.view(*dims[::-1])
+    want = torch.roll(xs, shifts=s0, dims=len(dims) - 1)
+    if len(dims) > 1:
+        want = torch.roll(want, shifts=2, dims=len(dims) - 2)
+    assert float(torch.linalg.vector_norm(y - want.reshape(-1)) / torch.linalg.vector_norm(x)) <= 1e-13
+    del want, xs
+    # linearity with a random filter
+    h = torch.complex(torch.randn(n, device="cuda", dtype=torch.float64, generator=g),
+                      torch.randn(n, device="cuda", dtype=torch.float64, generator=g))
+    f = pf.prepare_filter_from_impulse(h, plan)
+    x2 = torch.flip(x, dims=[0])
+    a, b = 0.75 - 0.5j, -1.25 + 0.25j
+    lhs = pf.convolve_permfree_out(a * x + b * x2, torch.empty_like(x), f, plan)
+    r1 = pf.convolve_permfree_out(x, torch.empty_like(x), f, plan)
+    r2 = pf.convolve_permfree_out(x2, x2, f, plan)  # in place
+    torch.cuda.synchronize()
+    assert float(torch.linalg.vector_norm(lhs - (a * r1 + b * r2)) / torch.linalg.vector_norm(lhs)) <= 1e-12
