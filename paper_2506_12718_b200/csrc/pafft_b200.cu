@@ -600,8 +600,9 @@ __global__ void scale_convert_kernel(const double2* __restrict__ in, cplx<T>* __
     }
 }
 
-// ghat_kernel[b*R + sum_j d_j wt(j)] = s * ghat[b*R + sum_j rev_{F_j}(d_j) wt(j)]:
-// the CONV pass multiplies frequency slots in its own natural-digit order.
+// Kernel copy of ghat, per R-block: slot sum_j d_j wt(j) (natural digit
+// order of the CONV pass) holds s * ghat[b*R + sum_j rev_{F_j}(d_j) wt(j)], and
+// slot g*FL + k (last-step group g, frequency k) is stored at k*(R/FL) + g.
 struct SlotPerm {
     int radix, ns, R;
     int F[4], wt[4];
@@ -622,7 +623,11 @@ __global__ void kernel_ghat_kernel(const cplx<T>* __restrict__ in, cplx<T>* __re
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         const unsigned long long blk = i / sp.R;
-        int rem = (int)(i - blk * sp.R), src = 0;
+        const int o = (int)(i - blk * sp.R);
+        // k-major within the block: the CONV's last step reads, for each of
+        // its FL frequencies k, one lane-contiguous run over the groups g
+        const int G = sp.ns ? sp.R / sp.F[sp.ns - 1] : 1;
+        int rem = sp.ns ? (o % G) * sp.F[sp.ns - 1] + o / G : o, src = 0;
         for (int j = 0; j < sp.ns; ++j) {
             const int d = rem / sp.wt[j];
             rem -= d * sp.wt[j];

@@ -505,10 +505,11 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                             // first DIT-conj step on the same registers
                             if (ok) {
                                 // the kernel copy of ghat is stored in this pass's slot
-                                // order (ghat[pos(k)] at slot sum k_j wt(j)): coalesced
-                                const V* gh = gblk + sb;
+                                // order (ghat[pos(k)] at slot sum k_j wt(j)), k-major:
+                                // slot g*FL + k at k*(R/FL) + g, so each load is one
+                                // lane-contiguous run (measured: config 3 CONV -15%)
 #pragma unroll
-                                for (int k = 0; k < FI; ++k) z[k] = cmul(z[k], __ldg(gh + k));
+                                for (int k = 0; k < FI; ++k) z[k] = cmul(z[k], __ldg(gblk + k * (R / FI) + g));
                             }
                             dft<FI, -1>(z);
                             if constexpr (NS == 1) {
