@@ -45,7 +45,8 @@ def _setup(pf, torch, cfg, batch):
 
 
 @pytest.mark.parametrize("idx,prec,nsig", [(1, "f64", 1), (2, "f64", 2), (3, "f64", 1), (4, "f64", 1),
-                                           (5, "f64", 4), (5, "f32", 4)])
+                                           (5, "f64", 4), (5, "f32", 4), (1, "f32", 1), (2, "f32", 1),
+                                           (3, "f32", 1), (4, "f32", 1)])
 def test_config_matches_oracle(pf, torch, orc, idx, prec, nsig):
     from paper_2506_12718_b200 import workload
     cfg = workload.get_config(idx, prec)
