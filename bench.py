@@ -447,7 +447,9 @@ def main():
                          "kernel": f"pass{dom}:{infos[dom]['kind']}(R={infos[dom]['R']})",
                          "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": pass_ms[dom],
                          "signals_per_launch": chunk,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         # what binds it (ncu --set full of the same kernel, committed)
+                         "ncu_pipes": ncu_traffic(f"config{cfg.idx}_{cfg.precision}_pipes")},
             "conv_roofline": {"bytes_per_conv": workload.bytes_per_conv(cfg, world), "achieved_gbs_per_gpu": conv_gbs,
                               "frac_of_hbm": conv_gbs / peak, "frac_of_hbm_datasheet_8tbs": conv_gbs / 8000.0,
                               "flops_per_conv": flops, "achieved_tflops_per_gpu": value / world * flops / 1e12,
