@@ -152,15 +152,23 @@ def cpu_comparator(cfg, count, threads):
     ghat = op.prepare_filter(op.filter_from_impulse(h))
     gr, gi = np.ascontiguousarray(ghat.real), np.ascontiguousarray(ghat.imag)
     re0, im0 = np.ascontiguousarray(xs.real), np.ascontiguousarray(xs.imag)
+    # radix 3/5 (not representable in pafft, core.hpp:14-19): pafft's ladder
+    # loop nest with a hand-expanded radix-r combine (oracle/fast_ladders.c);
+    # its radix-2 instance runs at pafft's own speed (tools/port_calibration.py)
+    fast = len(cfg.dims) == 1 and cfg.radix in (2, 3, 4, 5)
+    conv = op.convolve_permfree_fast_batch_split if fast else op.convolve_permfree_batch_split
 
     def run():
         re, im = re0.copy(), im0.copy()
         t = time.perf_counter()
-        op.convolve_permfree_batch_split(gr, gi, re, im, count, threads)
+        conv(gr, gi, re, im, count, threads)
         return time.perf_counter() - t
 
-    return run, "port", f"oracle restatement of pafft's ladders (radix {cfg.radix} is not representable in " \
-                        f"pafft, core.hpp:14-19), {count} signals of the workload"
+    what = ("pafft's ladder loop nest with a hand-expanded radix-%d combine (oracle/fast_ladders.c; its radix-2 "
+            "instance matches pafft's own speed, tools/port_calibration.py)" % cfg.radix) if fast else \
+        "oracle restatement of pafft's ladders"
+    return run, "port", f"{what}; radix {cfg.radix} is not representable in pafft (core.hpp:14-19); " \
+                        f"{count} signals of the workload"
 
 
 def cpu_threads():
@@ -173,8 +181,8 @@ def cpu_threads():
 def cpu_sample_count(cfg, threads):
     # bounded: ~10-30 s of CPU work at ~20 ns per point-stage per core
     work_per_conv = cfg.total * sum(cfg.stages) * 2 * 2e-8  # seconds per conv per core, rough
-    count = max(threads, int(round(15.0 / max(work_per_conv, 1e-6))))
-    return max(1, min(count, threads * 2, cfg.batch * cfg.calls))
+    count = max(threads, int(round(20.0 / max(work_per_conv, 1e-6))))
+    return max(1, min(count, threads * 4, cfg.batch * cfg.calls))
 
 
 def run_reference(args, cfg, rank):

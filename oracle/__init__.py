@@ -90,6 +90,7 @@ class Oracle:
         L.orc_fft_forward.argtypes = [C.POINTER(_OrcPlan), _dp, _dp]
         L.orc_fft_backward.argtypes = [C.POINTER(_OrcPlan), _dp, _dp]
         L.orc_convolve_permfree_batch.argtypes = [C.POINTER(_OrcPlan), _dp, _dp, _dp, _dp, _sz, C.c_int]
+        L.orc_convolve_permfree_fast_batch.argtypes = [C.POINTER(_OrcPlan), _dp, _dp, _dp, _dp, _sz, C.c_int]
         L.orc_naive_dft_tensor.argtypes = [C.POINTER(_sz), C.c_int, C.c_int, _dp, _dp, _dp, _dp]
         L.orc_naive_circular_convolution.argtypes = [C.POINTER(_sz), C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]
         L.orc_digit_reverse.argtypes = [C.c_uint64, C.c_uint, C.c_uint, C.POINTER(C.c_uint64)]
@@ -216,6 +217,15 @@ class OraclePlan:
         """In place on caller-owned split arrays (no copies): the CPU comparator."""
         return self.L.orc_convolve_permfree_batch(self.ptr, _p(ghat_re), _p(ghat_im), _p(re), _p(im),
                                                   batch, threads)
+
+    def convolve_permfree_fast_batch_split(self, ghat_re, ghat_im, re, im, batch, threads):
+        """Reference-style specialised ladders (fast_ladders.c; 1-D, radix 2/3/4/5):
+        the CPU stand-in for pafft at radix 3/5."""
+        st = self.L.orc_convolve_permfree_fast_batch(self.ptr, _p(ghat_re), _p(ghat_im), _p(re), _p(im),
+                                                     batch, threads)
+        if st:
+            raise OracleError(st, "convolve_permfree_fast_batch")
+        return st
 
 
 class Ref:

@@ -111,6 +111,14 @@ uint64_t orc_splitmix64_next(uint64_t* state);
 void orc_fill_uniform(uint64_t seed, size_t n, double* re, double* im);
 void orc_fill_normal(uint64_t seed, size_t n, double* re, double* im);
 
+/* Reference-style specialised ladders (fast_ladders.c): pafft's loop nest
+ * with a hand-expanded radix-r combine, r in {2,3,4,5}, 1-D plans.  The CPU
+ * stand-in for pafft at radix 3/5 in bench.py's reference arm. */
+int orc_convolve_permfree_fast(const orc_plan* p, const double* ghat_re, const double* ghat_im, double* re,
+                               double* im);
+int orc_convolve_permfree_fast_batch(const orc_plan* p, const double* ghat_re, const double* ghat_im, double* re,
+                                     double* im, size_t batch, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -290,3 +290,19 @@ def test_mixed_radix_oracle_pins(orc):
                           pu.convolve_permfree(x, pu.prepare_filter(pu.filter_from_impulse(h))))
     with pytest.raises(RuntimeError):
         orc.plan([3, 2], [27, 27])  # 27 is not a power of 2
+
+
+def test_reference_style_stand_in_matches_oracle(orc):
+    """oracle/fast_ladders.c -- the CPU stand-in bench.py times for pafft at
+    radix 3/5 -- computes the same convolution as the pinned restatement."""
+    for radix, n in [(2, 4096), (3, 3 ** 9), (4, 4096), (5, 5 ** 6), (3, 3), (5, 5)]:
+        x, h = rand_c(n, 91), rand_c(n, 92)
+        p = orc.plan(radix, [n])
+        gh = p.prepare_filter(p.filter_from_impulse(h))
+        want = p.convolve_permfree(x, gh)
+        xs = np.stack([x, x[::-1].copy()])
+        re, im = np.ascontiguousarray(xs.real), np.ascontiguousarray(xs.imag)
+        p.convolve_permfree_fast_batch_split(np.ascontiguousarray(gh.real), np.ascontiguousarray(gh.imag),
+                                             re, im, 2, 2)
+        assert rel_l2(re[0] + 1j * im[0], want) <= 1e-14
+        assert rel_l2(re[1] + 1j * im[1], p.convolve_permfree(x[::-1].copy(), gh)) <= 1e-14
