@@ -41,6 +41,15 @@
 #define PAFFT_MAX_MINB 4
 #endif
 
+// PAFFT_DEBUG builds (tools/debug_build.sh) check tile geometry and
+// shared-memory indices on the device; release builds compile them out.
+#ifdef PAFFT_DEBUG
+#include <cassert>
+#define PAFFT_DASSERT(c) assert(c)
+#else
+#define PAFFT_DASSERT(c) ((void)0)
+#endif
+
 namespace pafft_b200 {
 
 enum PassKind : int { KIND_DIF = 0, KIND_DIT_FWD = 1, KIND_DIT_CONJ = 2, KIND_CONV = 3 };
@@ -247,6 +256,10 @@ __device__ __forceinline__ TileGeo tile_geo(const PassArgs<T>& a, long long tile
         g.nvalid = left < W ? (int)left : W;
         g.base = (long long)p * a.panel_elems + g.first;
     }
+    PAFFT_DASSERT(g.nvalid >= 1 && g.nvalid <= W);
+    PAFFT_DASSERT(STRIDED ? (g.first + g.nvalid <= a.C && g.base + (long long)(R - 1) * a.C + g.nvalid <=
+                                                              a.panels * a.panel_elems)
+                          : (g.base + (long long)g.nvalid * R <= a.panels * a.panel_elems));
     return g;
 }
 
@@ -428,11 +441,14 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
         const int b0 = SHIFT && !a.use_tmap ? (int)(geo.base & 1) : 0;
         const int swx = a.swz;  // 0/1
         auto sref = [&](int row) -> V& {
+            PAFFT_DASSERT(row >= 0 && row < R);
             if constexpr (!STRIDED && (RADIX == 2 || RADIX == 4 || RADIX == 8)) {
                 const int e = c * R + row;
                 const int sw = sizeof(V) == 16 ? ((e >> 3) & 7) : (((e >> 4) & 7) << 1);
+                PAFFT_DASSERT((e ^ (sw & -swx)) < BUFE);
                 return buf[e ^ (sw & -swx)];
             } else {
+                PAFFT_DASSERT(&scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)] < bufs + 2 * BUFE);
                 return scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)];
             }
         };
