@@ -53,11 +53,15 @@ def _compile(src, verbose):
 def build(verbose: bool = False, jobs: int | None = None) -> str:
     os.makedirs(OBJ, exist_ok=True)
     hmt = _headers_mtime()
+    # objects are stale when the compiler flags changed (e.g. PAFFT_NVCC_EXTRA)
+    stamp = os.path.join(OBJ, "flags.txt")
+    flags = " ".join([NVCC, *ARCH, *FLAGS])
+    same_flags = os.path.exists(stamp) and open(stamp).read() == flags
     todo, objs = [], []
     for src in _sources():
         obj = _obj_for(src)
         objs.append(obj)
-        if not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hmt):
+        if not same_flags or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hmt):
             todo.append(src)
     if todo:
         jobs = jobs or min(len(todo), os.cpu_count() or 4)
@@ -65,6 +69,8 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
             for obj, log in ex.map(lambda s: _compile(s, verbose), todo):
                 if verbose and log:
                     print(log, file=sys.stderr)
+    with open(stamp, "w") as f:
+        f.write(flags)
     if todo or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
