@@ -16,8 +16,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libpafft_b200.so")
+# PAFFT_BUILD_TAG=<tag>: an A/B variant build (its own object dir, output
+# ab/lib<tag>.so), used with PAFFT_LIB=ab/lib<tag>.so
+_TAG = os.environ.get("PAFFT_BUILD_TAG", "")
+OBJ = os.path.join(HERE, "_build" + ("_" + _TAG if _TAG else ""))
+LIB = os.path.join(ROOT, "ab", "lib%s.so" % _TAG) if _TAG else os.path.join(HERE, "libpafft_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", *os.environ.get("PAFFT_NVCC_EXTRA", "").split(),
@@ -52,6 +55,7 @@ def _compile(src, verbose):
 
 def build(verbose: bool = False, jobs: int | None = None) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     hmt = _headers_mtime()
     # objects are stale when the compiler flags changed (e.g. PAFFT_NVCC_EXTRA)
     stamp = os.path.join(OBJ, "flags.txt")

@@ -179,8 +179,8 @@ struct pafft_plan_s {
     std::map<std::string, std::vector<const void*>> int_tables;            // split -> step tables
     std::map<long long, unsigned> ext_bits;
     std::vector<uint32_t*> rev_dev;            // per-axis digit reversal maps (device)
-    std::unique_ptr<DevBuf> stage[3];
-    cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+    std::unique_ptr<DevBuf> stage[4];
+    cudaStream_t streams[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaStream_t work[2] = {nullptr, nullptr};  // L2-chunk pipeline streams
     cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
     std::mutex mu;
@@ -1670,17 +1670,18 @@ pafft_status pafft_convolve_permfree_host_oop(pafft_plan_t p, pafft_filter_t f, 
     std::lock_guard<std::mutex> lk(p->host_mu);
     const size_t sig_bytes = p->total * p->esize;
     // chunks of ~64 MiB pipelined over three streams: H2D(i+1) || conv(i) || D2H(i-1)
-    size_t chunk = std::max<size_t>(1, (size_t)(64ull << 20) / sig_bytes);
+    const int ns = std::min(4, std::max(2, env_int("PAFFT_HOST_STREAMS", 3)));
+    size_t chunk = std::max<size_t>(1, ((size_t)env_int("PAFFT_HOST_CHUNK_MB", 64) << 20) / sig_bytes);
     chunk = std::min(chunk, batch);
-    for (auto& s : p->stage) ST_TRY(ensure(s, chunk * sig_bytes));
+    for (int i = 0; i < ns; ++i) ST_TRY(ensure(p->stage[i], chunk * sig_bytes));
     const char* src = (const char*)x_host;
     char* dst = (char*)y_host;
     size_t done = 0;
     int k = 0;
     while (done < batch) {
         const size_t nb = std::min(chunk, batch - done);
-        cudaStream_t st = p->streams[k % 3];
-        void* buf = p->stage[k % 3]->p;
+        cudaStream_t st = p->streams[k % ns];
+        void* buf = p->stage[k % ns]->p;
         CUDA_TRY(cudaMemcpyAsync(buf, src + done * sig_bytes, nb * sig_bytes, cudaMemcpyHostToDevice, st));
         ST_TRY(pafft_convolve_permfree(p, f, buf, nb, st));
         CUDA_TRY(cudaMemcpyAsync(dst + done * sig_bytes, buf, nb * sig_bytes, cudaMemcpyDeviceToHost, st));

@@ -40,6 +40,17 @@
 #ifndef PAFFT_MAX_MINB
 #define PAFFT_MAX_MINB 4
 #endif
+// Contiguous tiles single-buffered: more resident CTAs per SM instead of
+// double buffering inside one CTA.  0 = never, 1 = when double buffering
+// leaves one CTA per SM (measured on B200: config 1's R=4096 CONV, 1 -> 2 CTAs,
+// +5.6% conv/s; forcing it where two or more CTAs fit spills and loses 6-25%),
+// 2 = always (experiments).
+#ifndef PAFFT_SB
+#define PAFFT_SB 1
+#endif
+#ifndef PAFFT_SB_MAX_MINB
+#define PAFFT_SB_MAX_MINB 8
+#endif
 
 // PAFFT_DEBUG builds (tools/debug_build.sh) check tile geometry and
 // shared-memory indices on the device; release builds compile them out.
@@ -180,10 +191,18 @@ template <typename T, typename FAC, int MAP> struct TilePolicy {
     // (tensor-map destinations must be 128-byte aligned)
     // (tensor-map destinations 128-byte aligned, 128B-swizzled ones 1024)
     static constexpr int BUF = ((MAP == MAP_STRIDED ? FAC::R * SW : FAC::R * W) * ESZ + 1023) / 1024 * 1024;
-    static constexpr int SMEM = 2 * BUF + 16;
+    static constexpr int MINB_DB = (227 * 1024) / (2 * BUF + 16 + 1024);
+    static constexpr int NBUF = (MAP == MAP_CONTIG && (PAFFT_SB == 2 || (PAFFT_SB == 1 && MINB_DB <= 1))) ? 1 : 2;
+    static constexpr int SMEM = NBUF * BUF + 16;
     // resident CTAs per SM the shared memory allows (registers are capped to match)
     static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024);
-    static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > PAFFT_MAX_MINB ? PAFFT_MAX_MINB : MINB_SMEM);
+    // single-buffered CTAs are capped by registers instead: at least ~4 per
+    // complex value a thread holds (F_max of them) plus addressing
+    static constexpr int REG_FLOOR = FAC::FMAX >= 25 ? 128 : (FAC::FMAX >= 16 ? 96 : (FAC::FMAX >= 9 ? 72 : 64));
+    static constexpr int MINB_REG = 65536 / (((NT + 31) / 32 * 32) * REG_FLOOR);
+    static constexpr int MAXB = NBUF == 1 ? (MINB_REG < PAFFT_SB_MAX_MINB ? MINB_REG : PAFFT_SB_MAX_MINB)
+                                          : PAFFT_MAX_MINB;
+    static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > MAXB ? MAXB : MINB_SMEM);
 };
 
 template <typename T>
@@ -386,7 +405,8 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
     constexpr int NGL = FA::G(NS - 1) / GMIN;  // last-step groups per thread
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     V* const bufs = reinterpret_cast<V*>(smem_raw);
-    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem_raw + 2 * Pol::BUF);
+    constexpr int NBUF = Pol::NBUF;
+    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem_raw + NBUF * Pol::BUF);
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -406,7 +426,8 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
     const long long t0 = blockIdx.x, ts = gridDim.x;
     if (warp == 0) {
         if (t0 < a.tiles) stage_tile<R, W, SW, STRIDED>(a, &tmap, t0, bufs, &bars[0], lane);
-        if (t0 + ts < a.tiles) stage_tile<R, W, SW, STRIDED>(a, &tmap, t0 + ts, bufs + BUFE, &bars[1], lane);
+        if (NBUF == 2 && t0 + ts < a.tiles)
+            stage_tile<R, W, SW, STRIDED>(a, &tmap, t0 + ts, bufs + BUFE, &bars[1], lane);
     }
     __syncthreads();  // hand-copied fp32 tail elements of the first tiles
 
@@ -427,7 +448,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
     };
     int it = 0;
     for (long long tile = t0; tile < a.tiles; tile += ts, ++it) {
-        const int b = it & 1;
+        const int b = NBUF == 2 ? (it & 1) : 0;
         V* const buf = bufs + b * BUFE;
         const TileGeo geo = tile_geo<R, W, STRIDED>(a, tile);
         const long long first = geo.first;
@@ -448,7 +469,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                 PAFFT_DASSERT((e ^ (sw & -swx)) < BUFE);
                 return buf[e ^ (sw & -swx)];
             } else {
-                PAFFT_DASSERT(&scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)] < bufs + 2 * BUFE);
+                PAFFT_DASSERT(&scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)] < bufs + NBUF * BUFE);
                 return scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)];
             }
         };
@@ -459,7 +480,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
             tw = ext_root(a, jj * (unsigned long long)kf);
             st = ext_root(a, jj * (unsigned long long)S);
         };
-        mbar_wait(&bars[b], (it >> 1) & 1);
+        mbar_wait(&bars[b], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
 
         // hi index (digits 0..I-1 of a group) -> frequency offset sum k_j L(j)
         // and digit-reversed slot offset sum rev(k_j) wt(j); `rev_in` says the
@@ -647,12 +668,16 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
                 __syncwarp();
             }
         }
-        if (tile + 2 * ts < a.tiles) {
-            pend = tile + 2 * ts;
+        if (tile + NBUF * ts < a.tiles) {
+            pend = tile + NBUF * ts;
             pbuf = buf;
             pbar = &bars[b];
         }
-        if constexpr (!TSTORE || NS == 1) service();  // no later barrier in the next tile
+        // no later barrier in the next tile (or the next tile is this refill)
+        if constexpr (!TSTORE || NS == 1 || NBUF == 1) service();
+        // single buffer: an fp32 tail element hand-copied by the refill must be
+        // visible before the next tile's first shared-memory reads
+        if constexpr (NBUF == 1 && sizeof(V) == 8) __syncthreads();
     }
     service();
     if constexpr (TSTORE) {
