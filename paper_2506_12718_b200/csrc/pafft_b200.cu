@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/pafft_b200.h"
+#include "fused.cuh"
 #include "pass.cuh"
 #include "registry.h"
 
@@ -79,6 +80,13 @@ Registry& registry() {
         register_r5_f32(reg);
         register_r8_f32(reg);
     });
+    return reg;
+}
+
+FusedRegistry& fused_registry() {
+    static FusedRegistry reg;
+    static std::once_flag once;
+    std::call_once(once, [] { register_fused_f64(reg); });
     return reg;
 }
 
@@ -560,6 +568,131 @@ pafft_status launch(pafft_plan_t p, const PassDesc& d, const void* src, void* ds
                     const void* ghat, const void* mul, double scale, cudaStream_t st, long long grid_cap = 0) {
     return p->prec == 0 ? launch_t<double>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap)
                         : launch_t<float>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap);
+}
+
+// ------------------------------------------------ fused convolution --
+// One persistent launch for the three passes of a 1-D permutation-free plan
+// (fused.cuh).  Eligible: exactly DIF (strided) -> CONV -> DIT-conj (strided)
+// with a compiled fused instance for the (radix, R_strided, R_contig) pair.
+const FusedEntry* fused_entry(pafft_plan_t p) {
+    const std::vector<PassDesc>& ps = p->pf;
+    if (ps.size() != 3 || p->prec != 0) return nullptr;
+    if (ps[0].kind != KIND_DIF || ps[1].kind != KIND_CONV || ps[2].kind != KIND_DIT_CONJ) return nullptr;
+    if (ps[0].contig || !ps[1].contig || ps[2].contig || ps[0].R != ps[2].R || !ps[0].use_tmap || !ps[2].use_tmap)
+        return nullptr;
+    for (const auto& e : fused_registry())
+        if (e.prec == p->prec && e.radix == (int)p->radices[ps[0].axis] && e.RD == ps[0].R && e.RC == ps[1].R)
+            return &e;
+    return nullptr;
+}
+
+pafft_status launch_fused(pafft_plan_t p, const FusedEntry& fe, const void* ghat, const void* x, void* y,
+                          size_t batch, cudaStream_t st) {
+    using T = double;
+    const std::vector<PassDesc>& ps = p->pf;
+    FusedArgs<T> fa;
+    memset(&fa, 0, sizeof fa);
+    FusedMaps maps;
+    memset(&maps, 0, sizeof maps);
+    long long total_tiles = 0;
+    for (int i = 0; i < 3; ++i) {
+        PassDesc d = ps[i];
+        d.W = i == 1 ? fe.WC : fe.WD;
+        if (!d.contig) d.sw = d.W;
+        PassArgs<T>& a = fa.p[i];
+        const void* src = i == 0 ? x : (const void*)y;
+        a.src = (const cplx<T>*)src;
+        a.dst = (cplx<T>*)y;
+        const long long per_signal = (long long)p->total / ((long long)d.R * d.C);
+        a.panels = per_signal * (long long)batch;
+        a.panel_elems = (long long)d.R * d.C;
+        a.C = (int)d.C;
+        a.N = (long long)p->total;
+        a.ext = d.ext;
+        a.sq = (unsigned)d.sq;
+        a.ext_bits = d.ext_bits;
+        a.ext_lo = (const cplx<T>*)d.ext_lo;
+        a.ext_hi = (const cplx<T>*)d.ext_hi;
+        for (int k = 0; k < 3; ++k) a.tw[k] = (const cplx<T>*)d.tw[k];
+        a.scale = 1.0;
+        a.has_scale = 0;
+        long long U;
+        if (d.contig) {
+            // signal-major tiles: one run over the batch, W blocks per tile
+            if (per_signal % d.W) return fail(PAFFT_INVALID_ARGUMENT, "fused: blocks per signal %% W");
+            a.ghat = (const cplx<T>*)ghat;
+            a.nsig = 1;
+            a.bps = a.panels;
+            a.tiles_per_panel = 1;
+            a.tiles = a.panels / d.W;
+            U = per_signal / d.W;
+            a.swz = 0;
+            if (d.swz) {
+                const long long tile_bytes = (long long)d.R * d.W * (long long)p->esize;
+                if (tile_bytes % 1024 == 0) {
+                    const long long tr = tile_bytes / 128;
+                    a.swz_b1 = (int)std::min<long long>(tr, 256);
+                    a.swz = (tr % a.swz_b1 == 0 && tr / a.swz_b1 <= 256 &&
+                             ((long long)p->total * (long long)p->esize / 128) % a.swz_b1 == 0)
+                                ? 1
+                                : 0;
+                }
+                if (a.swz) {
+                    d.swz_b1 = a.swz_b1;
+                    ST_TRY(tensor_map_swz(p, d, src, batch, &maps.src[i]));
+                    ST_TRY(tensor_map_swz(p, d, y, batch, &maps.dst[i]));
+                }
+            }
+        } else {
+            a.nsig = (long long)batch;
+            a.bps = per_signal;
+            a.tiles_per_panel = (int)((d.C + d.W - 1) / d.W);
+            a.tiles = a.panels * a.tiles_per_panel;
+            U = per_signal * a.tiles_per_panel;
+            a.use_tmap = 1;
+            a.rb = d.rb;
+            ST_TRY(tensor_map(p, d, src, batch, &maps.src[i]));
+            ST_TRY(tensor_map(p, d, y, batch, &maps.dst[i]));
+        }
+        if (a.tiles > 0x7fffffffll) return fail(PAFFT_INVALID_ARGUMENT, "batch too large for one launch");
+        fa.U[i] = (int)U;
+        total_tiles += a.tiles;
+    }
+    static std::mutex attr_mu;
+    int occ = 0, sms = 0;
+    {
+        std::lock_guard<std::mutex> lk(attr_mu);
+        CUDA_TRY(cudaFuncSetAttribute(fe.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fe.smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fe.fn, fe.NT, fe.smem));
+    }
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+    if (occ < 1) return fail(PAFFT_CUDA_ERROR, "fused kernel cannot be resident");
+    const long long grid = std::max<long long>(1, std::min<long long>((long long)occ * sms, total_tiles));
+    // profiling aid: PAFFT_FUSED_ONLY=p runs only pass p's tiles through the
+    // fused machinery (the result is then not a convolution)
+    if (const int only = env_int("PAFFT_FUSED_ONLY", -1); only >= 0 && only < 3)
+        for (int i = 0; i < 3; ++i)
+            if (i != only) fa.U[i] = 0;
+    const int SU = fa.U[0] + fa.U[1] + fa.U[2];
+    // lag: enough tickets between a pass and its consumer that the consumer's
+    // dependency is normally complete when its tickets come up
+    const int lag = std::max(1, env_int("PAFFT_FUSED_LAG", (int)((2 * grid + SU - 1) / SU)));
+    fa.nsig = (int)batch;
+    fa.lag = lag;
+    fa.nticket = ((long long)batch + 2LL * lag) * SU;
+    // per-call counters (stream-ordered): concurrent calls never share them
+    const size_t cbytes = (1 + 3 * batch) * sizeof(unsigned);
+    void* cnt = nullptr;
+    CUDA_TRY(cudaMallocAsync(&cnt, cbytes, st));
+    CUDA_TRY(cudaMemsetAsync(cnt, 0, cbytes, st));
+    fa.ticket = (unsigned*)cnt;
+    fa.done = (unsigned*)cnt + 1;
+    void* args[] = {&fa, &maps};
+    const cudaError_t le = cudaLaunchKernel(fe.fn, dim3((unsigned)grid), dim3(fe.NT), args, fe.smem, st);
+    cudaFreeAsync(cnt, st);
+    CUDA_TRY(le);
+    ++g_launches;
+    return PAFFT_OK;
 }
 
 // ---------------------------------------------------- helper kernels --
@@ -1529,6 +1662,9 @@ pafft_status pafft_convolve_permfree_oop(pafft_plan_t p, pafft_filter_t f, const
     // measured on B200 (config 2): one-chunk launches lose more to tails than
     // L2 residency saves, so the chunk pipeline is opt-in (PAFFT_PIPELINE=1)
     const bool pipeline = ps.size() > 1 && batch > chunk && env_int("PAFFT_PIPELINE", 0) != 0;
+    if (env_int("PAFFT_FUSED", 0) != 0) {
+        if (const FusedEntry* fe = fused_entry(p)) return launch_fused(p, *fe, f->ghat_scaled->p, x_dev, y_dev, batch, st);
+    }
     if (!pipeline) {
         for (size_t i = 0; i < ps.size(); ++i)
             ST_TRY(launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch,

@@ -141,7 +141,7 @@ template <int F0, int F1, int F2, int F3> struct Fac {
 };
 
 // Compile-time tile policy shared by kernels and host plan (registry).
-template <typename T, typename FAC, int MAP> struct TilePolicy {
+template <typename T, typename FAC, int MAP, int WOVR = 0> struct TilePolicy {
     static constexpr int ESZ = (int)sizeof(cplx<T>);
     static constexpr int SMEM_BUDGET = 110 * 1024;  // per tile buffer (two are resident)
     // STRIDED: 8 (fp64) / 16 (fp32) columns = one 128-byte row segment; more
@@ -183,7 +183,7 @@ template <typename T, typename FAC, int MAP> struct TilePolicy {
             w = (w > 1 && FAC::R * (w + 1) * ESZ > SMEM_BUDGET) ? w - 1 : w + 1;
         return w;
     }
-    static constexpr int W = wcalc();
+    static constexpr int W = WOVR > 0 ? WOVR : wcalc();
     static constexpr int SW = rowslots(W);  // shared row stride (STRIDED)
     static constexpr int NT = FAC::GMIN * W;
     static_assert(NT >= 32, "tile policy needs a full warp");
@@ -383,18 +383,19 @@ __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorM
 // of a frequency index sits at rev(k_j) wt(j); CONV continues from the DIF's
 // natural frequency slots.  Every step reads and writes one slot set (in
 // place); the final spatial rows go to global memory with the epilogue.
-template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP>
-__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
-                                  TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::MINB)
-    pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap,
-                const __grid_constant__ CUtensorMap tmap_dst) {
+// One tile of a pass (the tile is staged in `buf`; the caller waited for it):
+// the column transforms, the epilogue, and the issue of the tile's bulk/tensor
+// store (committed as one bulk group by warp 0 lane 0).  `service` is called by
+// every thread after the tile's first internal barrier (the deferred refill).
+// Threads t >= Pol::NT (a fused kernel's wider CTA) only join the barriers.
+template <typename T, int RADIX, typename FA, int KIND, int MAP, typename Pol, bool ALL_ACTIVE, typename Svc>
+__device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap* tmap_dst, long long tile,
+                                         cplx<T>* buf, const cplx<T>* buf_end, int t, Svc&& service) {
     using V = cplx<T>;
-    using FA = Fac<F0, F1, F2, F3>;
-    using Pol = TilePolicy<T, FA, MAP>;
     constexpr int R = FA::R, NS = FA::NS, GMIN = FA::GMIN;
     constexpr int W = Pol::W;
     constexpr int SW = Pol::SW;
-    constexpr int BUFE = Pol::BUF / (int)sizeof(V);  // elements per tile buffer
+    constexpr int BUFE = Pol::BUF / (int)sizeof(V);
     constexpr bool STRIDED = MAP == MAP_STRIDED;
     constexpr bool SHIFT = Pol::SHIFT;
     constexpr int FL = FA::f(NS - 1);  // last codelet
@@ -403,6 +404,249 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
     // fp32 strided tiles (per-row shifted layout) keep register stores.
     constexpr bool TSTORE = !SHIFT;
     constexpr int NGL = FA::G(NS - 1) / GMIN;  // last-step groups per thread
+    (void)BUFE;
+    (void)buf_end;
+    const int warp = t >> 5, lane = t & 31;
+    const bool act = ALL_ACTIVE || t < Pol::NT;
+    // thread -> (tile column c, group slot gt); STRIDED: c fastest (coalesced
+    // W-wide row segments, conflict-free smem rows); CONTIG: group fastest.
+    const int c = STRIDED ? t % W : t / GMIN;
+    const int gt = STRIDED ? t / W : t % GMIN;
+    constexpr int SS = STRIDED ? SW : 1;  // shared stride between consecutive rows
+    const long long rs = STRIDED ? (long long)a.C : 1;  // global row stride
+    const TileGeo geo = tile_geo<R, W, STRIDED>(a, tile);
+    const long long first = geo.first;
+    // CONV: this column's filter block (the panel's position inside its signal)
+    const V* const gblk =
+        KIND == KIND_CONV ? a.ghat + (long long)((unsigned)(first + c) % (unsigned)(a.N / R)) * R : nullptr;
+    const bool ok = act && c < geo.nvalid;
+    V* const scol = STRIDED ? buf + c : buf + c * R;
+    // shared element of tile row `row` for this thread's column
+    const int codd = SHIFT && !a.use_tmap ? (a.C & 1) : 0;
+    const int b0 = SHIFT && !a.use_tmap ? (int)(geo.base & 1) : 0;
+    const int swx = a.swz;  // 0/1
+    auto sref = [&](int row) -> V& {
+        PAFFT_DASSERT(row >= 0 && row < R);
+        if constexpr (!STRIDED && (RADIX == 2 || RADIX == 4 || RADIX == 8)) {
+            const int e = c * R + row;
+            const int sw = sizeof(V) == 16 ? ((e >> 3) & 7) : (((e >> 4) & 7) << 1);
+            PAFFT_DASSERT((e ^ (sw & -swx)) < BUFE);
+            return buf[e ^ (sw & -swx)];
+        } else {
+            PAFFT_DASSERT(&scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)] < buf_end);
+            return scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)];
+        }
+    };
+    V* __restrict__ gdst = a.dst + geo.base + (STRIDED ? c : (long long)c * R);
+    // external twiddle base/step for this column: w_K0^{jj kf}, w_K0^{jj S}
+    auto ext_pair = [&](int kf, int S, V& tw, V& st) {
+        const unsigned long long jj = (unsigned long long)(first + c) / a.sq;
+        tw = ext_root(a, jj * (unsigned long long)kf);
+        st = ext_root(a, jj * (unsigned long long)S);
+    };
+
+    // hi index (digits 0..I-1 of a group) -> frequency offset sum k_j L(j)
+    // and digit-reversed slot offset sum rev(k_j) wt(j); `rev_in` says the
+    // slot digits are already reversed (DIT kinds).
+    auto hi_decode = [&](auto Ic, int hi, bool rev_in, int& kf, int& pos) {
+        constexpr int I = decltype(Ic)::value;
+        kf = 0;
+        pos = 0;
+        static_for<0, I>([&](auto jc) {
+            constexpr int jj = I - 1 - decltype(jc)::value;  // least significant digit first
+            constexpr int fj = FA::f(jj);
+            const int d = hi % fj;
+            hi /= fj;
+            const int k = rev_in ? revd<RADIX, fj>(d) : d;
+            kf += k * FA::L(jj);
+            pos += (rev_in ? d : revd<RADIX, fj>(d)) * FA::Q(jj);
+        });
+    };
+
+    // DIF results of the last step, held until every thread has read its
+    // last-step inputs (the output rows pos(k) belong to other groups)
+    V zl[KIND == KIND_DIF ? NGL : 1][KIND == KIND_DIF ? FL : 1];
+    int pl[KIND == KIND_DIF ? NGL : 1];
+    if constexpr (KIND == KIND_DIF || KIND == KIND_CONV) {
+        static_for<0, NS>([&](auto Ic) {
+            constexpr int I = decltype(Ic)::value;
+            constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
+            if constexpr (I > 0) __syncthreads();
+            if constexpr (I == 1) service();
+#pragma unroll
+            for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
+                const int g = gt + j * GMIN;
+                const int hi = g / QI, lo = g - (g / QI) * QI;
+                const int sb = hi * PI + lo;
+                V z[FI];
+#pragma unroll
+                for (int m = 0; m < FI; ++m) z[m] = sref(sb + m * QI);
+                dft<FI, 1>(z);
+                if constexpr (I < NS - 1) {
+                    // w_{P_I}^{k lo}: powers of tw[I][Q_I + lo] = w_{P_I}^{lo}
+                    twiddle_powers<FI, 1>(z, __ldg(a.tw[I] + QI + lo));
+#pragma unroll
+                    for (int k = 0; k < FI; ++k) sref(sb + k * QI) = z[k];
+                } else {
+                    // last DIF step (QI == 1, lo == 0): frequency kf + (R/FL) k
+                    int kf, pos;
+                    hi_decode(Ic, hi, false, kf, pos);
+                    if constexpr (KIND == KIND_DIF) {
+                        V tw{1, 0}, st{1, 0};
+                        if (a.ext && ok) ext_pair(kf, R / FL, tw, st);
+#pragma unroll
+                        for (int k = 0; k < FI; ++k) {
+                            zl[j][k] = a.ext ? cmul(z[k], tw) : z[k];
+                            if (a.ext) tw = cmul(tw, st);
+                        }
+                        pl[j] = pos;
+                    } else {
+                        // CONV: x ghat (digit-reversed, 1/N folded in), then the
+                        // first DIT-conj step on the same registers
+                        if (ok) {
+                            // the kernel copy of ghat is stored in this pass's slot
+                            // order (ghat[pos(k)] at slot sum k_j wt(j)), k-major:
+                            // slot g*FL + k at k*(R/FL) + g, so each load is one
+                            // lane-contiguous run (measured: config 3 CONV -15%)
+#pragma unroll
+                            for (int k = 0; k < FI; ++k) z[k] = cmul(z[k], __ldg(gblk + k * (R / FI) + g));
+                        }
+                        dft<FI, -1>(z);
+                        if constexpr (NS == 1) {
+                            if constexpr (TSTORE) {
+#pragma unroll
+                                for (int m = 0; m < FI; ++m) sref(m) = z[m];
+                            } else if (ok) {
+#pragma unroll
+                                for (int m = 0; m < FI; ++m) gdst[(long long)m * rs] = z[m];
+                            }
+                        } else {
+#pragma unroll
+                            for (int m = 0; m < FI; ++m) sref(sb + m) = z[m];
+                        }
+                    }
+                }
+            }
+        });
+    }
+
+    if constexpr (KIND == KIND_DIF) {
+        if constexpr (TSTORE) {
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < (act ? NGL : 0); ++j)
+#pragma unroll
+                for (int k = 0; k < FL; ++k) sref(pl[j] + revd<RADIX, FL>(k)) = zl[j][k];
+        } else if (ok) {
+#pragma unroll
+            for (int j = 0; j < NGL; ++j)
+#pragma unroll
+                for (int k = 0; k < FL; ++k) gdst[(long long)(pl[j] + revd<RADIX, FL>(k)) * rs] = zl[j][k];
+        }
+    }
+
+    if constexpr (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ || KIND == KIND_CONV) {
+        constexpr int S = (KIND == KIND_DIT_FWD) ? 1 : -1;
+        constexpr bool FIRST = KIND != KIND_CONV;  // slots hold digit-reversed frequency digits
+        auto tw = [](V x, V w) -> V { return S > 0 ? cmul(x, w) : cmulc(x, w); };
+        // DIT steps I = NS-1 .. 0 (CONV already did NS-1 in registers)
+        static_for<0, NS>([&](auto Rc) {
+            constexpr int I = NS - 1 - decltype(Rc)::value;
+            constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
+            if constexpr (!(KIND == KIND_CONV && I == NS - 1)) {
+                if constexpr (KIND == KIND_CONV || I < NS - 1) __syncthreads();
+                if constexpr (KIND != KIND_CONV && I == NS - 2) service();
+#pragma unroll
+                for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
+                    const int g = gt + j * GMIN;
+                    const int hi = g / QI, lo = g - (g / QI) * QI;
+                    const int sb = hi * PI + lo;
+                    V z[FI];
+#pragma unroll
+                    for (int k = 0; k < FI; ++k) z[k] = sref(sb + (FIRST ? revd<RADIX, FI>(k) : k) * QI);
+                    if constexpr (FIRST && I == NS - 1) {
+                        // pre-twiddle w_K0^{+-jj k} on the first DIT step
+                        if (a.ext && ok) {
+                            int kf, pos;
+                            hi_decode(std::integral_constant<int, I>{}, hi, true, kf, pos);
+                            V w, st;
+                            ext_pair(kf, R / FL, w, st);
+#pragma unroll
+                            for (int k = 0; k < FI; ++k) {
+                                z[k] = tw(z[k], w);
+                                w = cmul(w, st);
+                            }
+                        }
+                    }
+                    // pre-twiddle: the transpose of DIF step I's w_{P_I}^{k lo}
+                    if constexpr (I < NS - 1) twiddle_powers<FI, S>(z, __ldg(a.tw[I] + QI + lo));
+                    dft<FI, S>(z);
+                    if constexpr (I > 0) {
+#pragma unroll
+                        for (int m = 0; m < FI; ++m) sref(sb + m * QI) = z[m];
+                    } else {
+                        // final spatial rows m * Q_0 + lo (hi == 0), epilogue in registers
+                        V* gp = gdst + (long long)lo * rs;
+#pragma unroll
+                        for (int m = 0; m < FI; ++m) {
+                            V y = z[m];
+                            if (a.mul && ok) {
+                                const long long e = (gp - a.dst) + (long long)(m * QI) * rs;
+                                y = cmul(y, __ldg(a.mul + (e % a.N)));
+                            }
+                            if (a.has_scale) y = V{y.x * a.scale, y.y * a.scale};
+                            if constexpr (TSTORE) sref(sb + m * QI) = y;
+                            else if (ok) gp[(long long)(m * QI) * rs] = y;
+                        }
+                    }
+                }
+            }
+        });
+    }
+    // the tile is final in shared memory: one bulk/tensor store, then (once
+    // the store has read the buffer) refill it with tile it + 2
+    __syncthreads();
+    if (warp == 0) {
+        if constexpr (TSTORE) {
+            if (lane == 0) {
+                fence_proxy_async();
+                if constexpr (STRIDED) {
+                    const unsigned p = (unsigned)tile / (unsigned)a.tiles_per_panel;
+                    tma_store_3d(tmap_dst, buf, (int)(2 * first), 0, (int)(p * (R / a.rb)));
+                } else if (a.swz) {
+                    tma_store_3d(tmap_dst, buf, 0, 0, (int)(geo.base * (long long)sizeof(V) / 128 / a.swz_b1));
+                } else {
+                    const long long n = (long long)geo.nvalid * R;
+                    unsigned bytes = (unsigned)(n * sizeof(V));
+                    if constexpr (sizeof(V) == 8) {
+                        if (bytes & 15u) {  // odd fp32 element count: tail by hand
+                            bytes -= 8u;
+                            a.dst[geo.base + n - 1] = buf[n - 1];
+                        }
+                    }
+                    if (bytes) bulk_store_1d(a.dst + geo.base, buf, bytes);
+                }
+                bulk_commit();
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP>
+__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
+                                  TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::MINB)
+    pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                const __grid_constant__ CUtensorMap tmap_dst) {
+    using V = cplx<T>;
+    using FA = Fac<F0, F1, F2, F3>;
+    using Pol = TilePolicy<T, FA, MAP>;
+    constexpr int R = FA::R, NS = FA::NS;
+    constexpr int W = Pol::W;
+    constexpr int SW = Pol::SW;
+    constexpr int BUFE = Pol::BUF / (int)sizeof(V);  // elements per tile buffer
+    constexpr bool STRIDED = MAP == MAP_STRIDED;
+    constexpr bool TSTORE = !Pol::SHIFT;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     V* const bufs = reinterpret_cast<V*>(smem_raw);
     constexpr int NBUF = Pol::NBUF;
@@ -410,12 +654,6 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
-    // thread -> (tile column c, group slot gt); STRIDED: c fastest (coalesced
-    // W-wide row segments, conflict-free smem rows); CONTIG: group fastest.
-    const int c = STRIDED ? t % W : t / GMIN;
-    const int gt = STRIDED ? t / W : t % GMIN;
-    constexpr int SS = STRIDED ? SW : 1;  // shared stride between consecutive rows
-    const long long rs = STRIDED ? (long long)a.C : 1;  // global row stride
 
     if (t == 0) {
         mbar_init(&bars[0], 1);
@@ -450,224 +688,8 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
     for (long long tile = t0; tile < a.tiles; tile += ts, ++it) {
         const int b = NBUF == 2 ? (it & 1) : 0;
         V* const buf = bufs + b * BUFE;
-        const TileGeo geo = tile_geo<R, W, STRIDED>(a, tile);
-        const long long first = geo.first;
-        // CONV: this column's filter block (the panel's position inside its signal)
-        const V* const gblk =
-            KIND == KIND_CONV ? a.ghat + (long long)((unsigned)(first + c) % (unsigned)(a.N / R)) * R : nullptr;
-        const bool ok = c < geo.nvalid;
-        V* const scol = STRIDED ? buf + c : buf + c * R;
-        // shared element of tile row `row` for this thread's column
-        const int codd = SHIFT && !a.use_tmap ? (a.C & 1) : 0;
-        const int b0 = SHIFT && !a.use_tmap ? (int)(geo.base & 1) : 0;
-        const int swx = a.swz;  // 0/1
-        auto sref = [&](int row) -> V& {
-            PAFFT_DASSERT(row >= 0 && row < R);
-            if constexpr (!STRIDED && (RADIX == 2 || RADIX == 4 || RADIX == 8)) {
-                const int e = c * R + row;
-                const int sw = sizeof(V) == 16 ? ((e >> 3) & 7) : (((e >> 4) & 7) << 1);
-                PAFFT_DASSERT((e ^ (sw & -swx)) < BUFE);
-                return buf[e ^ (sw & -swx)];
-            } else {
-                PAFFT_DASSERT(&scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)] < bufs + NBUF * BUFE);
-                return scol[row * SS + (SHIFT ? ((row & codd) ^ b0) : 0)];
-            }
-        };
-        V* __restrict__ gdst = a.dst + geo.base + (STRIDED ? c : (long long)c * R);
-        // external twiddle base/step for this column: w_K0^{jj kf}, w_K0^{jj S}
-        auto ext_pair = [&](int kf, int S, V& tw, V& st) {
-            const unsigned long long jj = (unsigned long long)(first + c) / a.sq;
-            tw = ext_root(a, jj * (unsigned long long)kf);
-            st = ext_root(a, jj * (unsigned long long)S);
-        };
         mbar_wait(&bars[b], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
-
-        // hi index (digits 0..I-1 of a group) -> frequency offset sum k_j L(j)
-        // and digit-reversed slot offset sum rev(k_j) wt(j); `rev_in` says the
-        // slot digits are already reversed (DIT kinds).
-        auto hi_decode = [&](auto Ic, int hi, bool rev_in, int& kf, int& pos) {
-            constexpr int I = decltype(Ic)::value;
-            kf = 0;
-            pos = 0;
-            static_for<0, I>([&](auto jc) {
-                constexpr int jj = I - 1 - decltype(jc)::value;  // least significant digit first
-                constexpr int fj = FA::f(jj);
-                const int d = hi % fj;
-                hi /= fj;
-                const int k = rev_in ? revd<RADIX, fj>(d) : d;
-                kf += k * FA::L(jj);
-                pos += (rev_in ? d : revd<RADIX, fj>(d)) * FA::Q(jj);
-            });
-        };
-
-        // DIF results of the last step, held until every thread has read its
-        // last-step inputs (the output rows pos(k) belong to other groups)
-        V zl[KIND == KIND_DIF ? NGL : 1][KIND == KIND_DIF ? FL : 1];
-        int pl[KIND == KIND_DIF ? NGL : 1];
-        if constexpr (KIND == KIND_DIF || KIND == KIND_CONV) {
-            static_for<0, NS>([&](auto Ic) {
-                constexpr int I = decltype(Ic)::value;
-                constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
-                if constexpr (I > 0) __syncthreads();
-                if constexpr (I == 1) service();
-#pragma unroll
-                for (int j = 0; j < FA::G(I) / GMIN; ++j) {
-                    const int g = gt + j * GMIN;
-                    const int hi = g / QI, lo = g - (g / QI) * QI;
-                    const int sb = hi * PI + lo;
-                    V z[FI];
-#pragma unroll
-                    for (int m = 0; m < FI; ++m) z[m] = sref(sb + m * QI);
-                    dft<FI, 1>(z);
-                    if constexpr (I < NS - 1) {
-                        // w_{P_I}^{k lo}: powers of tw[I][Q_I + lo] = w_{P_I}^{lo}
-                        twiddle_powers<FI, 1>(z, __ldg(a.tw[I] + QI + lo));
-#pragma unroll
-                        for (int k = 0; k < FI; ++k) sref(sb + k * QI) = z[k];
-                    } else {
-                        // last DIF step (QI == 1, lo == 0): frequency kf + (R/FL) k
-                        int kf, pos;
-                        hi_decode(Ic, hi, false, kf, pos);
-                        if constexpr (KIND == KIND_DIF) {
-                            V tw{1, 0}, st{1, 0};
-                            if (a.ext && ok) ext_pair(kf, R / FL, tw, st);
-#pragma unroll
-                            for (int k = 0; k < FI; ++k) {
-                                zl[j][k] = a.ext ? cmul(z[k], tw) : z[k];
-                                if (a.ext) tw = cmul(tw, st);
-                            }
-                            pl[j] = pos;
-                        } else {
-                            // CONV: x ghat (digit-reversed, 1/N folded in), then the
-                            // first DIT-conj step on the same registers
-                            if (ok) {
-                                // the kernel copy of ghat is stored in this pass's slot
-                                // order (ghat[pos(k)] at slot sum k_j wt(j)), k-major:
-                                // slot g*FL + k at k*(R/FL) + g, so each load is one
-                                // lane-contiguous run (measured: config 3 CONV -15%)
-#pragma unroll
-                                for (int k = 0; k < FI; ++k) z[k] = cmul(z[k], __ldg(gblk + k * (R / FI) + g));
-                            }
-                            dft<FI, -1>(z);
-                            if constexpr (NS == 1) {
-                                if constexpr (TSTORE) {
-#pragma unroll
-                                    for (int m = 0; m < FI; ++m) sref(m) = z[m];
-                                } else if (ok) {
-#pragma unroll
-                                    for (int m = 0; m < FI; ++m) gdst[(long long)m * rs] = z[m];
-                                }
-                            } else {
-#pragma unroll
-                                for (int m = 0; m < FI; ++m) sref(sb + m) = z[m];
-                            }
-                        }
-                    }
-                }
-            });
-        }
-
-        if constexpr (KIND == KIND_DIF) {
-            if constexpr (TSTORE) {
-                __syncthreads();
-#pragma unroll
-                for (int j = 0; j < NGL; ++j)
-#pragma unroll
-                    for (int k = 0; k < FL; ++k) sref(pl[j] + revd<RADIX, FL>(k)) = zl[j][k];
-            } else if (ok) {
-#pragma unroll
-                for (int j = 0; j < NGL; ++j)
-#pragma unroll
-                    for (int k = 0; k < FL; ++k) gdst[(long long)(pl[j] + revd<RADIX, FL>(k)) * rs] = zl[j][k];
-            }
-        }
-
-        if constexpr (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ || KIND == KIND_CONV) {
-            constexpr int S = (KIND == KIND_DIT_FWD) ? 1 : -1;
-            constexpr bool FIRST = KIND != KIND_CONV;  // slots hold digit-reversed frequency digits
-            auto tw = [](V x, V w) -> V { return S > 0 ? cmul(x, w) : cmulc(x, w); };
-            // DIT steps I = NS-1 .. 0 (CONV already did NS-1 in registers)
-            static_for<0, NS>([&](auto Rc) {
-                constexpr int I = NS - 1 - decltype(Rc)::value;
-                constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
-                if constexpr (!(KIND == KIND_CONV && I == NS - 1)) {
-                    if constexpr (KIND == KIND_CONV || I < NS - 1) __syncthreads();
-                    if constexpr (KIND != KIND_CONV && I == NS - 2) service();
-#pragma unroll
-                    for (int j = 0; j < FA::G(I) / GMIN; ++j) {
-                        const int g = gt + j * GMIN;
-                        const int hi = g / QI, lo = g - (g / QI) * QI;
-                        const int sb = hi * PI + lo;
-                        V z[FI];
-#pragma unroll
-                        for (int k = 0; k < FI; ++k) z[k] = sref(sb + (FIRST ? revd<RADIX, FI>(k) : k) * QI);
-                        if constexpr (FIRST && I == NS - 1) {
-                            // pre-twiddle w_K0^{+-jj k} on the first DIT step
-                            if (a.ext && ok) {
-                                int kf, pos;
-                                hi_decode(std::integral_constant<int, I>{}, hi, true, kf, pos);
-                                V w, st;
-                                ext_pair(kf, R / FL, w, st);
-#pragma unroll
-                                for (int k = 0; k < FI; ++k) {
-                                    z[k] = tw(z[k], w);
-                                    w = cmul(w, st);
-                                }
-                            }
-                        }
-                        // pre-twiddle: the transpose of DIF step I's w_{P_I}^{k lo}
-                        if constexpr (I < NS - 1) twiddle_powers<FI, S>(z, __ldg(a.tw[I] + QI + lo));
-                        dft<FI, S>(z);
-                        if constexpr (I > 0) {
-#pragma unroll
-                            for (int m = 0; m < FI; ++m) sref(sb + m * QI) = z[m];
-                        } else {
-                            // final spatial rows m * Q_0 + lo (hi == 0), epilogue in registers
-                            V* gp = gdst + (long long)lo * rs;
-#pragma unroll
-                            for (int m = 0; m < FI; ++m) {
-                                V y = z[m];
-                                if (a.mul && ok) {
-                                    const long long e = (gp - a.dst) + (long long)(m * QI) * rs;
-                                    y = cmul(y, __ldg(a.mul + (e % a.N)));
-                                }
-                                if (a.has_scale) y = V{y.x * a.scale, y.y * a.scale};
-                                if constexpr (TSTORE) sref(sb + m * QI) = y;
-                                else if (ok) gp[(long long)(m * QI) * rs] = y;
-                            }
-                        }
-                    }
-                }
-            });
-        }
-        // the tile is final in shared memory: one bulk/tensor store, then (once
-        // the store has read the buffer) refill it with tile it + 2
-        __syncthreads();
-        if (warp == 0) {
-            if constexpr (TSTORE) {
-                if (lane == 0) {
-                    fence_proxy_async();
-                    if constexpr (STRIDED) {
-                        const unsigned p = (unsigned)tile / (unsigned)a.tiles_per_panel;
-                        tma_store_3d(&tmap_dst, buf, (int)(2 * first), 0, (int)(p * (R / a.rb)));
-                    } else if (a.swz) {
-                        tma_store_3d(&tmap_dst, buf, 0, 0, (int)(geo.base * (long long)sizeof(V) / 128 / a.swz_b1));
-                    } else {
-                        const long long n = (long long)geo.nvalid * R;
-                        unsigned bytes = (unsigned)(n * sizeof(V));
-                        if constexpr (sizeof(V) == 8) {
-                            if (bytes & 15u) {  // odd fp32 element count: tail by hand
-                                bytes -= 8u;
-                                a.dst[geo.base + n - 1] = buf[n - 1];
-                            }
-                        }
-                        if (bytes) bulk_store_1d(a.dst + geo.base, buf, bytes);
-                    }
-                    bulk_commit();
-                }
-                __syncwarp();
-            }
-        }
+        run_tile<T, RADIX, FA, KIND, MAP, Pol, true>(a, &tmap_dst, tile, buf, bufs + NBUF * BUFE, t, service);
         if (tile + NBUF * ts < a.tiles) {
             pend = tile + NBUF * ts;
             pbuf = buf;
