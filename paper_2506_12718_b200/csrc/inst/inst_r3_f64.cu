@@ -7,10 +7,10 @@ namespace pafft_b200 {
 // instances whose tile policy cannot launch (> 1024 threads or > 227 KB of
 // shared memory) are not registered; the plan then splits the axis further
 #define PAFFT_ENTRY(RADIX, F0, F1, F2, F3, KIND, MAP)                                                  \
-    if constexpr (TilePolicy<double, Fac<F0, F1, F2, F3>, MAP>::NT <= 1024 &&                                \
+    if constexpr (TilePolicy<double, Fac<F0, F1, F2, F3>, MAP>::NTB <= 1024 &&                                \
                   TilePolicy<double, Fac<F0, F1, F2, F3>, MAP>::SMEM <= 232448)                              \
         reg.push_back({0, RADIX, F0 * F1 * F2 * F3, F0, F1, F2, F3, KIND, MAP,                            \
-                       TilePolicy<double, Fac<F0, F1, F2, F3>, MAP>::W, TilePolicy<double, Fac<F0, F1, F2, F3>, MAP>::NT, \
+                       TilePolicy<double, Fac<F0, F1, F2, F3>, MAP>::W, TilePolicy<double, Fac<F0, F1, F2, F3>, MAP>::NTB, \
                        TilePolicy<double, Fac<F0, F1, F2, F3>, MAP>::SMEM,                                          \
                        (const void*)&pass_kernel<double, RADIX, F0, F1, F2, F3, KIND, MAP>});
 #define PAFFT_ADD(RADIX, F0, F1, F2, F3)                                     \

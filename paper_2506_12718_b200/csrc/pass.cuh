@@ -193,7 +193,7 @@ template <typename T, typename FAC, int MAP, int WOVR = 0> struct TilePolicy {
     static constexpr int BUF = ((MAP == MAP_STRIDED ? FAC::R * SW : FAC::R * W) * ESZ + 1023) / 1024 * 1024;
     static constexpr int MINB_DB = (227 * 1024) / (2 * BUF + 16 + 1024);
     static constexpr int NBUF = (MAP == MAP_CONTIG && (PAFFT_SB == 2 || (PAFFT_SB == 1 && MINB_DB <= 1))) ? 1 : 2;
-    static constexpr int SMEM = NBUF * BUF + 16;
+    static constexpr int SMEM = NBUF * BUF + 32;
     // resident CTAs per SM the shared memory allows (registers are capped to match)
     static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024);
     // single-buffered CTAs are capped by registers instead: at least ~4 per
@@ -203,6 +203,7 @@ template <typename T, typename FAC, int MAP, int WOVR = 0> struct TilePolicy {
     static constexpr int MAXB = NBUF == 1 ? (MINB_REG < PAFFT_SB_MAX_MINB ? MINB_REG : PAFFT_SB_MAX_MINB)
                                           : PAFFT_MAX_MINB;
     static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > MAXB ? MAXB : MINB_SMEM);
+    static constexpr int NTB = NT;  // threads per block
 };
 
 template <typename T>
@@ -383,14 +384,51 @@ __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorM
 // of a frequency index sits at rev(k_j) wt(j); CONV continues from the DIF's
 // natural frequency slots.  Every step reads and writes one slot set (in
 // place); the final spatial rows go to global memory with the epilogue.
+// The tile's bulk/tensor store from shared memory, committed as one bulk group
+// (called by one thread).
+template <typename T, int R, int W, bool STRIDED>
+__device__ __forceinline__ void issue_tile_store(const PassArgs<T>& a, const CUtensorMap* tmap_dst, long long tile,
+                                                 cplx<T>* buf) {
+    using V = cplx<T>;
+    const TileGeo geo = tile_geo<R, W, STRIDED>(a, tile);
+    fence_proxy_async();
+    if constexpr (STRIDED) {
+        const unsigned p = (unsigned)tile / (unsigned)a.tiles_per_panel;
+        tma_store_3d(tmap_dst, buf, (int)(2 * geo.first), 0, (int)(p * (R / a.rb)));
+    } else if (a.swz) {
+        (void)W;
+        tma_store_3d(tmap_dst, buf, 0, 0, (int)(geo.base * (long long)sizeof(V) / 128 / a.swz_b1));
+    } else {
+        const long long n = (long long)geo.nvalid * R;
+        unsigned bytes = (unsigned)(n * sizeof(V));
+        if constexpr (sizeof(V) == 8) {
+            if (bytes & 15u) {  // odd fp32 element count: tail by hand
+                bytes -= 8u;
+                a.dst[geo.base + n - 1] = buf[n - 1];
+            }
+        }
+        if (bytes) bulk_store_1d(a.dst + geo.base, buf, bytes);
+    }
+    bulk_commit();
+}
+
+// Tile-internal barrier: the whole CTA, or (SYNCN > 0, warp-specialised) the
+// SYNCN compute threads on named barrier 1.
+template <int SYNCN> __device__ __forceinline__ void tile_sync() {
+    if constexpr (SYNCN > 0) asm volatile("bar.sync 1, %0;" ::"n"(SYNCN) : "memory");
+    else __syncthreads();
+}
+
 // One tile of a pass (the tile is staged in `buf`; the caller waited for it):
 // the column transforms, the epilogue, and the issue of the tile's bulk/tensor
 // store (committed as one bulk group by warp 0 lane 0).  `service` is called by
 // every thread after the tile's first internal barrier (the deferred refill).
 // Threads t >= Pol::NT (a fused kernel's wider CTA) only join the barriers.
-template <typename T, int RADIX, typename FA, int KIND, int MAP, typename Pol, bool ALL_ACTIVE, typename Svc>
+template <typename T, int RADIX, typename FA, int KIND, int MAP, typename Pol, bool ALL_ACTIVE, int SYNCN,
+          typename Svc>
 __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap* tmap_dst, long long tile,
-                                         cplx<T>* buf, const cplx<T>* buf_end, int t, Svc&& service) {
+                                         cplx<T>* buf, const cplx<T>* buf_end, int t, Svc&& service,
+                                         unsigned long long* done_bar = nullptr) {
     using V = cplx<T>;
     constexpr int R = FA::R, NS = FA::NS, GMIN = FA::GMIN;
     constexpr int W = Pol::W;
@@ -471,7 +509,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
         static_for<0, NS>([&](auto Ic) {
             constexpr int I = decltype(Ic)::value;
             constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
-            if constexpr (I > 0) __syncthreads();
+            if constexpr (I > 0) tile_sync<SYNCN>();
             if constexpr (I == 1) service();
 #pragma unroll
             for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
@@ -532,7 +570,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
 
     if constexpr (KIND == KIND_DIF) {
         if constexpr (TSTORE) {
-            __syncthreads();
+            tile_sync<SYNCN>();
 #pragma unroll
             for (int j = 0; j < (act ? NGL : 0); ++j)
 #pragma unroll
@@ -554,7 +592,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
             constexpr int I = NS - 1 - decltype(Rc)::value;
             constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
             if constexpr (!(KIND == KIND_CONV && I == NS - 1)) {
-                if constexpr (KIND == KIND_CONV || I < NS - 1) __syncthreads();
+                if constexpr (KIND == KIND_CONV || I < NS - 1) tile_sync<SYNCN>();
                 if constexpr (KIND != KIND_CONV && I == NS - 2) service();
 #pragma unroll
                 for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
@@ -603,38 +641,25 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
             }
         });
     }
-    // the tile is final in shared memory: one bulk/tensor store, then (once
-    // the store has read the buffer) refill it with tile it + 2
-    __syncthreads();
-    if (warp == 0) {
-        if constexpr (TSTORE) {
-            if (lane == 0) {
-                fence_proxy_async();
-                if constexpr (STRIDED) {
-                    const unsigned p = (unsigned)tile / (unsigned)a.tiles_per_panel;
-                    tma_store_3d(tmap_dst, buf, (int)(2 * first), 0, (int)(p * (R / a.rb)));
-                } else if (a.swz) {
-                    tma_store_3d(tmap_dst, buf, 0, 0, (int)(geo.base * (long long)sizeof(V) / 128 / a.swz_b1));
-                } else {
-                    const long long n = (long long)geo.nvalid * R;
-                    unsigned bytes = (unsigned)(n * sizeof(V));
-                    if constexpr (sizeof(V) == 8) {
-                        if (bytes & 15u) {  // odd fp32 element count: tail by hand
-                            bytes -= 8u;
-                            a.dst[geo.base + n - 1] = buf[n - 1];
-                        }
-                    }
-                    if (bytes) bulk_store_1d(a.dst + geo.base, buf, bytes);
-                }
-                bulk_commit();
+    // the tile is final in shared memory: one bulk/tensor store (by warp 0,
+    // or -- warp-specialised -- by the producer warp once every compute thread
+    // has arrived on `done_bar`)
+    if constexpr (SYNCN > 0) {
+        fence_proxy_async();
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(done_bar)) : "memory");
+    } else {
+        __syncthreads();
+        if (warp == 0) {
+            if constexpr (TSTORE) {
+                if (lane == 0) issue_tile_store<T, R, W, STRIDED>(a, tmap_dst, tile, buf);
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
 }
 
 template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP>
-__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
+__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
                                   TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::MINB)
     pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap,
                 const __grid_constant__ CUtensorMap tmap_dst) {
@@ -689,7 +714,8 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NT,
         const int b = NBUF == 2 ? (it & 1) : 0;
         V* const buf = bufs + b * BUFE;
         mbar_wait(&bars[b], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
-        run_tile<T, RADIX, FA, KIND, MAP, Pol, true>(a, &tmap_dst, tile, buf, bufs + NBUF * BUFE, t, service);
+        run_tile<T, RADIX, FA, KIND, MAP, Pol, Pol::NTB == Pol::NT, 0>(a, &tmap_dst, tile, buf, bufs + NBUF * BUFE, t,
+                                                                    service);
         if (tile + NBUF * ts < a.tiles) {
             pend = tile + NBUF * ts;
             pbuf = buf;
