@@ -1707,8 +1707,10 @@ pafft_status pafft_convolve_permfree_pass(pafft_plan_t p, pafft_filter_t f, cons
     }
     if (i < 0 || i >= (int)ps.size()) return fail(PAFFT_INVALID_ARGUMENT, "pass index %d out of range", i);
     ST_TRY(set_device(p));
+    // profiling aid: PAFFT_PASS_GRID_CAP limits the persistent grid (co-running
+    // passes on disjoint SM sets, tools/corun_probe.py)
     return launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch, ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr,
-                  nullptr, 1.0, (cudaStream_t)stream);
+                  nullptr, 1.0, (cudaStream_t)stream, env_int("PAFFT_PASS_GRID_CAP", 0));
 }
 
 size_t pafft_plan_chunk_signals(pafft_plan_t p) {
