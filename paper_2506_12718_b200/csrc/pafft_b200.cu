@@ -1276,6 +1276,9 @@ pafft_status pafft_filter_sync_scaled(pafft_filter_t f, void* stream) {
     sp.ns = 0;
     if (!p->pf.empty()) {
         const PassDesc& cv = p->pf[p->pf.size() / 2];  // the CONV pass
+        // the CONV pass's own axis radix: it is axis 0's only when axis 0 has
+        // extent > 1 (with leading extent-1 axes it is the first longer axis)
+        sp.radix = (int)p->radices[cv.axis];
         sp.R = cv.R;
         sp.ns = cv.nsteps;
         int w = 1;
