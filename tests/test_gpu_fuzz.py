@@ -75,3 +75,49 @@ def test_random_plan_matches_oracle(env, orc, radices, dims, batch, f32, mid):
     gd = torch.from_numpy(np.asarray(g).reshape(-1)).to("cuda", cdt)
     ys = pf.convolve_standard_(x.clone(), gd, plan).cpu().numpy().astype(np.complex128)
     assert max(rel_l2(ys[b], want[b]) for b in range(batch)) <= bar
+
+
+def _case_large(seed):
+    rng = np.random.default_rng(5000 + seed)
+    rank = int(rng.integers(1, 4))
+    radices, dims = [], []
+    budget = 20.0
+    for q in range(rank):
+        r = int(rng.choice(RADICES))
+        tmax = int(budget / np.log2(r))
+        t = int(rng.integers(1 if q == 0 else 0, max(1, tmax) + 1)) if tmax > 0 else 0
+        radices.append(r)
+        dims.append(r ** t)
+        budget -= t * np.log2(r)
+    return radices, dims, int(rng.integers(1, 3)), bool(rng.random() < 0.3), bool(rng.random() < 0.5)
+
+
+LARGE = [_case_large(s) for s in range(24)]
+
+
+@pytest.mark.parametrize("radices,dims,batch,f32,inplace", LARGE, ids=[str(c) for c in LARGE])
+def test_random_large_plan_matches_oracle(env, orc, radices, dims, batch, f32, inplace):
+    """Up to 2^20 points per signal: multi-pass schedules on every axis, in place
+    or out of place, and the drop-in host split API for batch 1."""
+    pf, torch = env
+    n = int(np.prod(dims))
+    prec = pf.F32 if f32 else pf.F64
+    cdt = torch.complex64 if f32 else torch.complex128
+    bar = 1e-5 if f32 else 1e-12
+    xs = np.stack([rand_c(n, 11 * n + b) for b in range(batch)])
+    h = rand_c(n, 5 * n + 3)
+    if f32:
+        xs = xs.astype(np.complex64).astype(np.complex128)
+        h = h.astype(np.complex64).astype(np.complex128)
+    plan = pf.Plan(radices, dims, precision=prec)
+    op = orc.plan(list(radices), dims)
+    gh = op.prepare_filter(op.filter_from_impulse(h))
+    want = [op.convolve_permfree(xs[b], gh) for b in range(batch)]
+    filt = pf.prepare_filter_from_impulse(torch.from_numpy(h).to("cuda", cdt), plan)
+    x = torch.from_numpy(xs).to("cuda", cdt)
+    if inplace:
+        y = pf.convolve_permfree_(x, filt, plan)
+    else:
+        y = pf.convolve_permfree_out(x, torch.empty_like(x), filt, plan)
+    y = y.cpu().numpy().astype(np.complex128)
+    assert max(rel_l2(y[b], want[b]) for b in range(batch)) <= bar
