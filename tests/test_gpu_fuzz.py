@@ -98,7 +98,7 @@ LARGE = [_case_large(s) for s in range(24)]
 @pytest.mark.parametrize("radices,dims,batch,f32,inplace", LARGE, ids=[str(c) for c in LARGE])
 def test_random_large_plan_matches_oracle(env, orc, radices, dims, batch, f32, inplace):
     """Up to 2^20 points per signal: multi-pass schedules on every axis, in place
-    or out of place, and the drop-in host split API for batch 1."""
+    or out of place."""
     pf, torch = env
     n = int(np.prod(dims))
     prec = pf.F32 if f32 else pf.F64
@@ -121,3 +121,32 @@ def test_random_large_plan_matches_oracle(env, orc, radices, dims, batch, f32, i
         y = pf.convolve_permfree_out(x, torch.empty_like(x), filt, plan)
     y = y.cpu().numpy().astype(np.complex128)
     assert max(rel_l2(y[b], want[b]) for b in range(batch)) <= bar
+
+
+@pytest.mark.parametrize("radices,dims,batch,f32,mid", CASES[:32], ids=[str(c) for c in CASES[:32]])
+def test_random_plan_transforms_match_oracle(env, orc, radices, dims, batch, f32, mid):
+    """The device transforms of the same random plans (fp64): natural-order
+    forward/backward, the bare ladders (A, A-bar, A^T) and the explicit
+    permutation (bit-exact) against the oracle's (transform.cpp:8-26,
+    butterfly.cpp:423-466, permutation.cpp:46-90)."""
+    pf, torch = env
+    n = int(np.prod(dims))
+    xs = np.stack([rand_c(n, 13 * n + b) for b in range(batch)])
+    plan = pf.Plan(radices, dims, precision=pf.F64)
+    op = orc.plan(list(radices), dims)
+    x = torch.from_numpy(xs).to("cuda", torch.complex128)
+
+    def dev(fn):
+        return fn(x.clone(), plan).cpu().numpy()
+
+    def check(got, fn, bar=1e-12):
+        for b in range(batch):
+            assert rel_l2(got[b], fn(xs[b])) <= bar
+    check(dev(pf.fft_forward_), op.fft_forward)
+    check(dev(pf.fft_backward_), op.fft_backward)
+    check(dev(pf.fft_transposed_), lambda v: op.butterfly_tensor(v, 2))
+    check(dev(pf.fft_forward_unordered_), lambda v: op.butterfly_tensor(v, 0))
+    check(dev(pf.fft_backward_unordered_), lambda v: op.butterfly_tensor(v, 1) / n)
+    got = dev(pf.permute_)
+    for b in range(batch):
+        assert np.array_equal(got[b], op.permute(xs[b]))
