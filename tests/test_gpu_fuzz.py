@@ -150,3 +150,25 @@ def test_random_plan_transforms_match_oracle(env, orc, radices, dims, batch, f32
     got = dev(pf.permute_)
     for b in range(batch):
         assert np.array_equal(got[b], op.permute(xs[b]))
+
+
+@pytest.mark.parametrize("radices,dims,batch,f32,mid", CASES[:24], ids=[str(c) for c in CASES[:24]])
+def test_random_plan_dropin_host_api(env, orc, radices, dims, batch, f32, mid):
+    """The reference-shaped host API (numpy C-order arrays, module.cpp:73-149):
+    prepare_filter is bit-exact (one permutation of the natural spectrum), the
+    device-side prepare-from-impulse equals it, and convolve_permfree on host
+    arrays matches the oracle."""
+    pf, torch = env
+    n = int(np.prod(dims))
+    plan = pf.Plan(radices, dims, precision=pf.F64)
+    op = orc.plan(list(radices), dims)
+    h = rand_c(n, 17 * n + 1)
+    g = op.filter_from_impulse(h)                       # vec order
+    gh = op.prepare_filter(g)
+    filt = pf.prepare_filter(g.reshape(dims, order="F"), plan)
+    assert np.array_equal(filt.ghat, gh)
+    fdev = pf.prepare_filter_from_impulse(torch.from_numpy(h).to("cuda", torch.complex128), plan)
+    assert rel_l2(fdev.ghat, gh) <= 1e-13
+    x = rand_c(n, 19 * n + 2)
+    y = pf.convolve_permfree(x.reshape(dims, order="F"), filt, plan)
+    assert rel_l2(np.asarray(y).reshape(-1, order="F"), op.convolve_permfree(x, gh)) <= 1e-12
