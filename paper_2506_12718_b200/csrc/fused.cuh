@@ -236,13 +236,13 @@ __global__ void __launch_bounds__((FusedShape<T, RADIX, D0, D1, D2, D3, WD, C0, 
         };
         auto service = [&]() { service_impl(std::false_type{}); };
         if (J.p == 1)
-            run_tile<T, RADIX, FC, KIND_CONV, MAP_CONTIG, PC, PC::NT == SH::NT, 0>(fa.p[1], &maps.dst[1], J.tile, buf,
+            run_tile<T, RADIX, FC, KIND_CONV, MAP_CONTIG, PC, PC::NT == SH::NT>(fa.p[1], &maps.dst[1], J.tile, buf,
                                                                                bufs + 2 * BUFE, t, service);
         else if (J.p == 0)
-            run_tile<T, RADIX, FD, KIND_DIF, MAP_STRIDED, PD, PD::NT == SH::NT, 0>(fa.p[0], &maps.dst[0], J.tile, buf,
+            run_tile<T, RADIX, FD, KIND_DIF, MAP_STRIDED, PD, PD::NT == SH::NT>(fa.p[0], &maps.dst[0], J.tile, buf,
                                                                                bufs + 2 * BUFE, t, service);
         else
-            run_tile<T, RADIX, FD, KIND_DIT_CONJ, MAP_STRIDED, PD, PD::NT == SH::NT, 0>(fa.p[2], &maps.dst[2], J.tile,
+            run_tile<T, RADIX, FD, KIND_DIT_CONJ, MAP_STRIDED, PD, PD::NT == SH::NT>(fa.p[2], &maps.dst[2], J.tile,
                                                                                     buf, bufs + 2 * BUFE, t, service);
         if (!serviced) service_impl(std::true_type{});
         if (t == 0) pb = J;

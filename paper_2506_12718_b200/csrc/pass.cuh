@@ -439,23 +439,14 @@ __device__ __forceinline__ void issue_tile_store(const PassArgs<T>& a, const CUt
     bulk_commit();
 }
 
-// Tile-internal barrier: the whole CTA, or (SYNCN > 0, warp-specialised) the
-// SYNCN compute threads on named barrier 1.
-template <int SYNCN> __device__ __forceinline__ void tile_sync() {
-    if constexpr (SYNCN > 0) asm volatile("bar.sync 1, %0;" ::"n"(SYNCN) : "memory");
-    else __syncthreads();
-}
-
 // One tile of a pass (the tile is staged in `buf`; the caller waited for it):
 // the column transforms, the epilogue, and the issue of the tile's bulk/tensor
 // store (committed as one bulk group by warp 0 lane 0).  `service` is called by
 // every thread after the tile's first internal barrier (the deferred refill).
 // Threads t >= Pol::NT (a fused kernel's wider CTA) only join the barriers.
-template <typename T, int RADIX, typename FA, int KIND, int MAP, typename Pol, bool ALL_ACTIVE, int SYNCN,
-          typename Svc>
+template <typename T, int RADIX, typename FA, int KIND, int MAP, typename Pol, bool ALL_ACTIVE, typename Svc>
 __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap* tmap_dst, long long tile,
-                                         cplx<T>* buf, const cplx<T>* buf_end, int t, Svc&& service,
-                                         unsigned long long* done_bar = nullptr) {
+                                         cplx<T>* buf, const cplx<T>* buf_end, int t, Svc&& service) {
     using V = cplx<T>;
     constexpr int R = FA::R, NS = FA::NS, GMIN = FA::GMIN;
     constexpr int W = Pol::W;
@@ -536,7 +527,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
         static_for<0, NS>([&](auto Ic) {
             constexpr int I = decltype(Ic)::value;
             constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
-            if constexpr (I > 0) tile_sync<SYNCN>();
+            if constexpr (I > 0) __syncthreads();
             if constexpr (I == 1) service();
 #pragma unroll
             for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
@@ -597,7 +588,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
 
     if constexpr (KIND == KIND_DIF) {
         if constexpr (TSTORE) {
-            tile_sync<SYNCN>();
+            __syncthreads();
 #pragma unroll
             for (int j = 0; j < (act ? NGL : 0); ++j)
 #pragma unroll
@@ -619,7 +610,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
             constexpr int I = NS - 1 - decltype(Rc)::value;
             constexpr int FI = FA::f(I), PI = FA::P(I), QI = FA::Q(I);
             if constexpr (!(KIND == KIND_CONV && I == NS - 1)) {
-                if constexpr (KIND == KIND_CONV || I < NS - 1) tile_sync<SYNCN>();
+                if constexpr (KIND == KIND_CONV || I < NS - 1) __syncthreads();
                 if constexpr (KIND != KIND_CONV && I == NS - 2) service();
 #pragma unroll
                 for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
@@ -668,19 +659,12 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
             }
         });
     }
-    // the tile is final in shared memory: one bulk/tensor store (by warp 0,
-    // or -- warp-specialised -- by the producer warp once every compute thread
-    // has arrived on `done_bar`)
-    if constexpr (SYNCN > 0) {
-        fence_proxy_async();
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(done_bar)) : "memory");
-    } else {
-        __syncthreads();
-        if (warp == 0) {
-            if constexpr (TSTORE) {
-                if (lane == 0) issue_tile_store<T, R, W, STRIDED>(a, tmap_dst, tile, buf);
-                __syncwarp();
-            }
+    // the tile is final in shared memory: one bulk/tensor store by warp 0
+    __syncthreads();
+    if (warp == 0) {
+        if constexpr (TSTORE) {
+            if (lane == 0) issue_tile_store<T, R, W, STRIDED>(a, tmap_dst, tile, buf);
+            __syncwarp();
         }
     }
 }
@@ -743,7 +727,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
         const int b = NBUF == 2 ? (it & 1) : 0;
         V* const buf = bufs + b * BUFE;
         mbar_wait(&bars[b], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
-        run_tile<T, RADIX, FA, KIND, MAP, Pol, Pol::NTB == Pol::NT, 0>(a, &tmap_dst, tile, buf, bufs + NBUF * BUFE, t,
+        run_tile<T, RADIX, FA, KIND, MAP, Pol, Pol::NTB == Pol::NT>(a, &tmap_dst, tile, buf, bufs + NBUF * BUFE, t,
                                                                     service);
         if (tile + NBUF * ts < a.tiles) {
             pend = tile + NBUF * ts;
