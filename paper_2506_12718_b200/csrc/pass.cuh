@@ -439,6 +439,32 @@ __device__ __forceinline__ void issue_tile_store(const PassArgs<T>& a, const CUt
     bulk_commit();
 }
 
+// Steps whose inner index lo = g mod Q_I takes only a few values (Q_I <= 3,
+// codelets of <= 9 points, one group per thread): threads are mapped lo-major,
+// so lo is uniform across most warps, and the twiddle w_{P_I}^{k lo} is applied
+// as compile-time constants for each lo (none for lo = 0) instead of powers of
+// a table value.  Measured on B200: config 2's CONV pass -3.5% time; with
+// 25-point codelets (config 5) the per-lo code copies cost more than they save.
+#ifndef PAFFT_SMALLQ
+#define PAFFT_SMALLQ 1
+#endif
+template <typename FA, int I> struct SmallQ {
+    static constexpr bool on = PAFFT_SMALLQ && I < FA::NS - 1 && FA::Q(I) > 1 && FA::Q(I) <= 3 &&
+                               FA::f(I) <= 9 && FA::G(I) == FA::GMIN;
+};
+template <int F, int P, int L, int S, typename V> __device__ __forceinline__ void twiddle_lo(V (&z)[F]) {
+    static_for<1, F>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        z[k] = twiddle_const<P, k * L, S>(z[k]);
+    });
+}
+template <int F, int P, int Q, int S, typename V> __device__ __forceinline__ void twiddle_small_q(V (&z)[F], int lo) {
+    static_for<1, Q>([&](auto lc) {
+        constexpr int L = decltype(lc)::value;
+        if (lo == L) twiddle_lo<F, P, L, S>(z);
+    });
+}
+
 // One tile of a pass (the tile is staged in `buf`; the caller waited for it):
 // the column transforms, the epilogue, and the issue of the tile's bulk/tensor
 // store (committed as one bulk group by warp 0 lane 0).  `service` is called by
@@ -531,7 +557,8 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
             if constexpr (I == 1) service();
 #pragma unroll
             for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
-                const int g = gt + j * GMIN;
+                constexpr bool SQ = SmallQ<FA, I>::on;
+                const int g = SQ ? (gt % (FA::G(I) / QI)) * QI + gt / (FA::G(I) / QI) : gt + j * GMIN;
                 const int hi = g / QI, lo = g - (g / QI) * QI;
                 const int sb = hi * PI + lo;
                 V z[FI];
@@ -540,7 +567,8 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                 dft<FI, 1>(z);
                 if constexpr (I < NS - 1) {
                     // w_{P_I}^{k lo}: powers of tw[I][Q_I + lo] = w_{P_I}^{lo}
-                    twiddle_powers<FI, 1>(z, __ldg(a.tw[I] + QI + lo));
+                    if constexpr (SQ) twiddle_small_q<FI, PI, QI, 1>(z, lo);
+                    else twiddle_powers<FI, 1>(z, __ldg(a.tw[I] + QI + lo));
 #pragma unroll
                     for (int k = 0; k < FI; ++k) sref(sb + k * QI) = z[k];
                 } else {
@@ -614,7 +642,8 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                 if constexpr (KIND != KIND_CONV && I == NS - 2) service();
 #pragma unroll
                 for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
-                    const int g = gt + j * GMIN;
+                    constexpr bool SQ = SmallQ<FA, I>::on;
+                    const int g = SQ ? (gt % (FA::G(I) / QI)) * QI + gt / (FA::G(I) / QI) : gt + j * GMIN;
                     const int hi = g / QI, lo = g - (g / QI) * QI;
                     const int sb = hi * PI + lo;
                     V z[FI];
@@ -635,7 +664,10 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                         }
                     }
                     // pre-twiddle: the transpose of DIF step I's w_{P_I}^{k lo}
-                    if constexpr (I < NS - 1) twiddle_powers<FI, S>(z, __ldg(a.tw[I] + QI + lo));
+                    if constexpr (I < NS - 1) {
+                        if constexpr (SQ) twiddle_small_q<FI, PI, QI, S>(z, lo);
+                        else twiddle_powers<FI, S>(z, __ldg(a.tw[I] + QI + lo));
+                    }
                     dft<FI, S>(z);
                     if constexpr (I > 0) {
 #pragma unroll
