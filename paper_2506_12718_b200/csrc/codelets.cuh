@@ -221,17 +221,43 @@ template <int P, int S, typename V> __device__ __forceinline__ void dft(V (&z)[P
     }
 }
 
-// z[k] *= w^(k) for k = 1 .. F-1 (S = -1: conj(w)^k), w^k built by binary
-// powering in registers (error ~ log2(F) roundings) instead of F-1 table loads.
+// z[k] *= w^(k) for k = 1 .. F-1 (S = -1: conj(w)^k).  Codelets of fewer
+// than PAFFT_CHEB_MIN points build w^k by binary powering in registers (error
+// ~ log2(F) roundings); larger ones by the Chebyshev three-term recurrence
+// w^{k+1} = 2 cos(theta) w^k - w^{k-1} (|w| = 1): two FMAs per power instead
+// of a complex multiply, on a longer dependency chain.  Measured on B200 with
+// the threshold at 16: config 1 +4%, config 5 +2.3%, config 2 neutral, but
+// config 3 -2.8% and config 4 -10% (16-point CONV tiles at 12 warps/SM cannot
+// hide the chain), so it is used from 25 points on (config 5's codelets).
+// The recurrence's error grows ~k cot(theta) ulps: config 5 1.1e-14 relative
+// L2 vs 1.9e-15 with binary powering, against the 1e-12 bar
+// (tools/accuracy_probe.py).
+#ifndef PAFFT_CHEB_MIN
+#define PAFFT_CHEB_MIN 25
+#endif
 template <int F, int S, typename V> __device__ __forceinline__ void twiddle_powers(V (&z)[F], V w) {
     if constexpr (F > 1) {
         if constexpr (S < 0) w.y = -w.y;
-        V p[F];
-        p[1] = w;
+        if constexpr (F >= PAFFT_CHEB_MIN) {
+            using T = decltype(w.x);
+            const T c2 = w.x + w.x;
+            V pm{(T)1, (T)0}, pc = w;
+            z[1] = cmul(z[1], w);
 #pragma unroll
-        for (int k = 2; k < F; ++k) p[k] = (k & 1) ? cmul(p[k - 1], p[1]) : cmul(p[k / 2], p[k / 2]);
+            for (int k = 2; k < F; ++k) {
+                const V pn{c2 * pc.x - pm.x, c2 * pc.y - pm.y};
+                z[k] = cmul(z[k], pn);
+                pm = pc;
+                pc = pn;
+            }
+        } else {
+            V p[F];
+            p[1] = w;
 #pragma unroll
-        for (int k = 1; k < F; ++k) z[k] = cmul(z[k], p[k]);
+            for (int k = 2; k < F; ++k) p[k] = (k & 1) ? cmul(p[k - 1], p[1]) : cmul(p[k / 2], p[k / 2]);
+#pragma unroll
+            for (int k = 1; k < F; ++k) z[k] = cmul(z[k], p[k]);
+        }
     }
 }
 
