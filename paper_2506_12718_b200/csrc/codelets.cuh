@@ -228,17 +228,20 @@ template <int P, int S, typename V> __device__ __forceinline__ void dft(V (&z)[P
 // of a complex multiply, on a longer dependency chain.  Measured on B200 with
 // the threshold at 16: config 1 +4%, config 5 +2.3%, config 2 neutral, but
 // config 3 -2.8% and config 4 -10% (16-point CONV tiles at 12 warps/SM cannot
-// hide the chain), so it is used from 25 points on (config 5's codelets).
+// hide the chain), so it is used from 25 points on (config 5's codelets), and
+// from 16 points in contiguous tiles of >= 256 threads (CHEB16: config 1,
+// +3.3%, 5.2e-15 relative L2).
 // The recurrence's error grows ~k cot(theta) ulps: config 5 1.1e-14 relative
 // L2 vs 1.9e-15 with binary powering, against the 1e-12 bar
 // (tools/accuracy_probe.py).
 #ifndef PAFFT_CHEB_MIN
 #define PAFFT_CHEB_MIN 25
 #endif
-template <int F, int S, typename V> __device__ __forceinline__ void twiddle_powers(V (&z)[F], V w) {
+template <int F, int S, bool CHEB16 = false, typename V>
+__device__ __forceinline__ void twiddle_powers(V (&z)[F], V w) {
     if constexpr (F > 1) {
         if constexpr (S < 0) w.y = -w.y;
-        if constexpr (F >= PAFFT_CHEB_MIN) {
+        if constexpr (F >= PAFFT_CHEB_MIN || (CHEB16 && F >= 16)) {
             using T = decltype(w.x);
             const T c2 = w.x + w.x;
             V pm{(T)1, (T)0}, pc = w;

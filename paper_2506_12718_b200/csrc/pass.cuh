@@ -486,6 +486,9 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     // fp32 strided tiles (per-row shifted layout) keep register stores.
     constexpr bool TSTORE = !SHIFT;
     constexpr int NGL = FA::G(NS - 1) / GMIN;  // last-step groups per thread
+    // Chebyshev twiddle powers for 16-point steps (codelets.cuh) where enough
+    // warps hide its longer chain: contiguous tiles of >= 256 threads
+    constexpr bool CHEB16 = !STRIDED && Pol::NT >= 256;
     (void)BUFE;
     (void)buf_end;
     const int warp = t >> 5, lane = t & 31;
@@ -568,7 +571,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                 if constexpr (I < NS - 1) {
                     // w_{P_I}^{k lo}: powers of tw[I][Q_I + lo] = w_{P_I}^{lo}
                     if constexpr (SQ) twiddle_small_q<FI, PI, QI, 1>(z, lo);
-                    else twiddle_powers<FI, 1>(z, __ldg(a.tw[I] + QI + lo));
+                    else twiddle_powers<FI, 1, CHEB16>(z, __ldg(a.tw[I] + QI + lo));
 #pragma unroll
                     for (int k = 0; k < FI; ++k) sref(sb + k * QI) = z[k];
                 } else {
@@ -666,7 +669,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                     // pre-twiddle: the transpose of DIF step I's w_{P_I}^{k lo}
                     if constexpr (I < NS - 1) {
                         if constexpr (SQ) twiddle_small_q<FI, PI, QI, S>(z, lo);
-                        else twiddle_powers<FI, S>(z, __ldg(a.tw[I] + QI + lo));
+                        else twiddle_powers<FI, S, CHEB16>(z, __ldg(a.tw[I] + QI + lo));
                     }
                     dft<FI, S>(z);
                     if constexpr (I > 0) {
