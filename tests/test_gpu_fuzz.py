@@ -172,3 +172,23 @@ def test_random_plan_dropin_host_api(env, orc, radices, dims, batch, f32, mid):
     x = rand_c(n, 19 * n + 2)
     y = pf.convolve_permfree(x.reshape(dims, order="F"), filt, plan)
     assert rel_l2(np.asarray(y).reshape(-1, order="F"), op.convolve_permfree(x, gh)) <= 1e-12
+
+
+@pytest.mark.parametrize("radices,dims,batch,f32,mid", CASES[:24], ids=[str(c) for c in CASES[:24]])
+def test_random_plan_host_buffer_path_bitwise(env, radices, dims, batch, f32, mid):
+    """The host-buffer entry point (pinned H2D, convolve, D2H pipelined over
+    streams; the e2e leg of bench.py) gives exactly the device path's result,
+    fp32 odd lengths included."""
+    pf, torch = env
+    n = int(np.prod(dims))
+    prec = pf.F32 if f32 else pf.F64
+    cdt = torch.complex64 if f32 else torch.complex128
+    xs = np.stack([rand_c(n, 23 * n + b) for b in range(batch)])
+    h = rand_c(n, 29 * n + 1)
+    plan = pf.Plan(radices, dims, precision=prec)
+    filt = pf.prepare_filter_from_impulse(torch.from_numpy(h).to("cuda", cdt), plan)
+    x = torch.from_numpy(xs).to(cdt)
+    ydev = pf.convolve_permfree_out(x.cuda(), torch.empty_like(x, device="cuda"), filt, plan).cpu()
+    xp = x.pin_memory()
+    pf.convolve_permfree_host(xp.numpy(), filt, plan)  # in place on the pinned buffer
+    assert torch.equal(xp, ydev)
