@@ -48,6 +48,9 @@
 #ifndef PAFFT_SB
 #define PAFFT_SB 1
 #endif
+#ifndef PAFFT_GHAT_PF
+#define PAFFT_GHAT_PF 1
+#endif
 #ifndef PAFFT_SB_MAX_MINB
 #define PAFFT_SB_MAX_MINB 8
 #endif
@@ -754,6 +757,21 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
             fence_proxy_async();
             stage_tile<R, W, SW, STRIDED>(a, &tmap, pend, pbuf, pbar, lane);
             if (PAFFT_L2PF && lane == 0 && pend + ts < a.tiles) prefetch_tile_l2<R, W, STRIDED>(a, &tmap, pend + ts);
+            if constexpr (KIND == KIND_CONV && PAFFT_GHAT_PF && FA::FMAX < 25) {
+                // the staged tile's filter blocks into L2 ahead of the multiply:
+                // measured on B200 config 4 (256 MiB filter) CONV -9%, config 2
+                // (24 MiB) -2%; a filter of a few MiB stays in L2 anyway (size
+                // floor), and the instruction-cache-bound 25-point kernels
+                // (config 5) lose ~1% to the extra code, so they skip it
+                if (lane == 0 && a.N * (long long)sizeof(V) >= (8ll << 20)) {
+                    const TileGeo g = tile_geo<R, W, STRIDED>(a, pend);
+                    const long long nb = a.N / R, b0 = g.first % nb;
+                    const long long nblk = b0 + g.nvalid <= nb ? g.nvalid : nb - b0;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.ghat + b0 * R),
+                                 "r"((unsigned)(nblk * R * sizeof(V)))
+                                 : "memory");
+                }
+            }
         }
         pend = -1;
     };
