@@ -48,6 +48,9 @@
 #ifndef PAFFT_SB
 #define PAFFT_SB 1
 #endif
+#ifndef PAFFT_EXT_HOIST
+#define PAFFT_EXT_HOIST 1
+#endif
 #ifndef PAFFT_GHAT_PF
 #define PAFFT_GHAT_PF 1
 #endif
@@ -475,7 +478,8 @@ template <int F, int P, int Q, int S, typename V> __device__ __forceinline__ voi
 // Threads t >= Pol::NT (a fused kernel's wider CTA) only join the barriers.
 template <typename T, int RADIX, typename FA, int KIND, int MAP, typename Pol, bool ALL_ACTIVE, typename Svc>
 __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap* tmap_dst, long long tile,
-                                         cplx<T>* buf, const cplx<T>* buf_end, int t, Svc&& service) {
+                                         cplx<T>* buf, const cplx<T>* buf_end, int t, Svc&& service,
+                                         unsigned long long* tile_bar = nullptr, unsigned tile_phase = 0) {
     using V = cplx<T>;
     constexpr int R = FA::R, NS = FA::NS, GMIN = FA::GMIN;
     constexpr int W = Pol::W;
@@ -550,6 +554,25 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
             pos += (rev_in ? d : revd<RADIX, fj>(d)) * FA::Q(jj);
         });
     };
+
+    // DIT kinds: the first step's external twiddle pair w_K0^{jj kf}, w_K0^{jj S}
+    // is loaded before waiting for the tile, so the table latency hides under
+    // the TMA wait (PAFFT_EXT_HOIST)
+    constexpr int NJF = FA::G(NS - 1) / GMIN;
+    constexpr bool HOIST =
+        PAFFT_EXT_HOIST && STRIDED && (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ) && NJF <= 2;
+    V hw[HOIST ? NJF : 1], hs[HOIST ? NJF : 1];
+    if constexpr (HOIST) {
+        if (a.ext && ok) {
+#pragma unroll
+            for (int j = 0; j < NJF; ++j) {
+                int kf, pos;
+                hi_decode(std::integral_constant<int, NS - 1>{}, gt + j * GMIN, true, kf, pos);
+                ext_pair(kf, R / FL, hw[j], hs[j]);
+            }
+        }
+    }
+    if (tile_bar) mbar_wait(tile_bar, tile_phase);
 
     // DIF results of the last step, held until every thread has read its
     // last-step inputs (the output rows pos(k) belong to other groups)
@@ -658,10 +681,15 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                     if constexpr (FIRST && I == NS - 1) {
                         // pre-twiddle w_K0^{+-jj k} on the first DIT step
                         if (a.ext && ok) {
-                            int kf, pos;
-                            hi_decode(std::integral_constant<int, I>{}, hi, true, kf, pos);
                             V w, st;
-                            ext_pair(kf, R / FL, w, st);
+                            if constexpr (HOIST) {
+                                w = hw[j];
+                                st = hs[j];
+                            } else {
+                                int kf, pos;
+                                hi_decode(std::integral_constant<int, I>{}, hi, true, kf, pos);
+                                ext_pair(kf, R / FL, w, st);
+                            }
 #pragma unroll
                             for (int k = 0; k < FI; ++k) {
                                 z[k] = tw(z[k], w);
@@ -779,9 +807,9 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
     for (long long tile = t0; tile < a.tiles; tile += ts, ++it) {
         const int b = NBUF == 2 ? (it & 1) : 0;
         V* const buf = bufs + b * BUFE;
-        mbar_wait(&bars[b], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
         run_tile<T, RADIX, FA, KIND, MAP, Pol, Pol::NTB == Pol::NT>(a, &tmap_dst, tile, buf, bufs + NBUF * BUFE, t,
-                                                                    service);
+                                                                    service, &bars[b],
+                                                                    NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
         if (tile + NBUF * ts < a.tiles) {
             pend = tile + NBUF * ts;
             pbuf = buf;
