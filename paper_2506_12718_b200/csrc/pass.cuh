@@ -559,10 +559,11 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     // is loaded before waiting for the tile, so the table latency hides under
     // the TMA wait (PAFFT_EXT_HOIST)
     constexpr int NJF = FA::G(NS - 1) / GMIN;
-    // (full 128-byte-row tiles only: config 3's 2-column tiles, which never
-    // carry an external twiddle, measured 2% slower from the extra code)
-    constexpr bool HOIST =
-        PAFFT_EXT_HOIST && STRIDED && (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ) && NJF <= 2 && W >= 8;
+    // (fp64 tiles of full 128-byte rows only: config 3's 2-column tiles, which
+    // never carry an external twiddle, measured 2% slower from the extra code,
+    // and config 5's fp32 DIT 12% slower)
+    constexpr bool HOIST = PAFFT_EXT_HOIST && STRIDED && sizeof(V) == 16 &&
+                           (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ) && NJF <= 2 && W >= 8;
     V hw[HOIST ? NJF : 1], hs[HOIST ? NJF : 1];
     if constexpr (HOIST) {
         if (a.ext && ok) {
