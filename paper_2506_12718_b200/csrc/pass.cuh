@@ -51,6 +51,11 @@
 #ifndef PAFFT_EXT_HOIST
 #define PAFFT_EXT_HOIST 1
 #endif
+// DIT ext hoisting only for codelets of <= 9 points (config 1's 16-point DIT
+// measured 0.5% faster without it)
+#ifndef PAFFT_HOIST_FMAX
+#define PAFFT_HOIST_FMAX 9
+#endif
 #ifndef PAFFT_GHAT_PF
 #define PAFFT_GHAT_PF 1
 #endif
@@ -563,7 +568,8 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     // never carry an external twiddle, measured 2% slower from the extra code,
     // and config 5's fp32 DIT 12% slower)
     constexpr bool HOIST = PAFFT_EXT_HOIST && STRIDED && sizeof(V) == 16 &&
-                           (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ) && NJF <= 2 && W >= 8;
+                           (KIND == KIND_DIT_FWD || KIND == KIND_DIT_CONJ) && NJF <= 2 && W >= 8 &&
+                           FA::FMAX <= PAFFT_HOIST_FMAX;
     V hw[HOIST ? NJF : 1], hs[HOIST ? NJF : 1];
     if constexpr (HOIST) {
         if (a.ext && ok) {
