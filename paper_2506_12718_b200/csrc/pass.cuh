@@ -721,11 +721,14 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
 #pragma unroll
                         for (int m = 0; m < FI; ++m) {
                             V y = z[m];
-                            if (a.mul && ok) {
-                                const long long e = (gp - a.dst) + (long long)(m * QI) * rs;
-                                y = cmul(y, __ldg(a.mul + (e % a.N)));
+                            // (the CONV pass never has an epilogue: 1/N is in its filter copy)
+                            if constexpr (KIND != KIND_CONV) {
+                                if (a.mul && ok) {
+                                    const long long e = (gp - a.dst) + (long long)(m * QI) * rs;
+                                    y = cmul(y, __ldg(a.mul + (e % a.N)));
+                                }
+                                if (a.has_scale) y = V{y.x * a.scale, y.y * a.scale};
                             }
-                            if (a.has_scale) y = V{y.x * a.scale, y.y * a.scale};
                             if constexpr (TSTORE) sref(sb + m * QI) = y;
                             else if (ok) gp[(long long)(m * QI) * rs] = y;
                         }
