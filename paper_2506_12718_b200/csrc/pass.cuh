@@ -476,6 +476,18 @@ template <int F, int P, int Q, int S, typename V> __device__ __forceinline__ voi
     });
 }
 
+// DIT epilogue of the transforms and the standard-order comparator (natural-
+// order multiplier of period N, then a scale), kept out of line.
+#ifndef PAFFT_EPI_CALL
+#define PAFFT_EPI_CALL 1
+#endif
+template <typename T>
+__device__ __noinline__ cplx<T> dit_epilogue(const PassArgs<T>& a, cplx<T> y, long long e, bool ok) {
+    if (a.mul && ok) y = cmul(y, __ldg(a.mul + (e % a.N)));
+    if (a.has_scale) y = cplx<T>{y.x * a.scale, y.y * a.scale};
+    return y;
+}
+
 // One tile of a pass (the tile is staged in `buf`; the caller waited for it):
 // the column transforms, the epilogue, and the issue of the tile's bulk/tensor
 // store (committed as one bulk group by warp 0 lane 0).  `service` is called by
@@ -723,11 +735,17 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                             V y = z[m];
                             // (the CONV pass never has an epilogue: 1/N is in its filter copy)
                             if constexpr (KIND != KIND_CONV) {
+#if PAFFT_EPI_CALL
+                                // out of line: the permutation-free passes never take it
+                                if (a.mul || a.has_scale)
+                                    y = dit_epilogue(a, y, (gp - a.dst) + (long long)(m * QI) * rs, ok);
+#else
                                 if (a.mul && ok) {
                                     const long long e = (gp - a.dst) + (long long)(m * QI) * rs;
                                     y = cmul(y, __ldg(a.mul + (e % a.N)));
                                 }
                                 if (a.has_scale) y = V{y.x * a.scale, y.y * a.scale};
+#endif
                             }
                             if constexpr (TSTORE) sref(sb + m * QI) = y;
                             else if (ok) gp[(long long)(m * QI) * rs] = y;
