@@ -626,12 +626,19 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                     int kf, pos;
                     hi_decode(Ic, hi, false, kf, pos);
                     if constexpr (KIND == KIND_DIF) {
-                        V tw{1, 0}, st{1, 0};
-                        if (a.ext && ok) ext_pair(kf, R / FL, tw, st);
+                        // external twiddle w_K0^{jj k} (a uniform branch: passes
+                        // over a whole axis have none)
+                        if (a.ext) {
+                            V tw{1, 0}, st{1, 0};
+                            if (ok) ext_pair(kf, R / FL, tw, st);
 #pragma unroll
-                        for (int k = 0; k < FI; ++k) {
-                            zl[j][k] = a.ext ? cmul(z[k], tw) : z[k];
-                            if (a.ext) tw = cmul(tw, st);
+                            for (int k = 0; k < FI; ++k) {
+                                zl[j][k] = cmul(z[k], tw);
+                                tw = cmul(tw, st);
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < FI; ++k) zl[j][k] = z[k];
                         }
                         pl[j] = pos;
                     } else {
