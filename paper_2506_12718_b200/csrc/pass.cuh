@@ -350,6 +350,34 @@ __device__ __forceinline__ void prefetch_tile_l2(const PassArgs<T>& a, const CUt
     }
 }
 
+template <int R, int W, int SW, typename T>
+__device__ __noinline__ void stage_rows(const PassArgs<T>& a, const TileGeo g, cplx<T>* buf, unsigned long long* bar,
+                                        int lane) {
+    using V = cplx<T>;
+    const V* src = a.src + g.base;
+    if constexpr (sizeof(V) == 16) {
+        const unsigned rb = (unsigned)(g.nvalid * sizeof(V));
+        if (lane == 0) mbar_expect_tx(bar, rb * R);
+        __syncwarp();
+        for (int j = lane; j < R; j += 32) tma_load_1d(buf + j * SW, src + (long long)j * a.C, rb, bar);
+    } else {
+        // total bytes: sum over rows of round16(shift_j*8 + nvalid*8)
+        const long long b0 = g.base & 1;
+        const unsigned odd = (unsigned)(a.C & 1);
+        const unsigned n8 = (unsigned)g.nvalid * 8u;
+        const unsigned sz0 = (n8 + 15u) & ~15u;              // shift 0
+        const unsigned sz1 = (n8 + 8u + 15u) & ~15u;         // shift 1
+        const unsigned rows_shift1 = odd ? (unsigned)(b0 ? (R + 1) / 2 : R / 2) : (unsigned)(b0 ? R : 0);
+        if (lane == 0) mbar_expect_tx(bar, rows_shift1 * sz1 + ((unsigned)R - rows_shift1) * sz0);
+        __syncwarp();
+        for (int j = lane; j < R; j += 32) {
+            const unsigned sh = (unsigned)(b0 ^ (j & odd));
+            const V* row = src + (long long)j * a.C - sh;
+            tma_load_1d(buf + j * SW, row, sh ? sz1 : sz0, bar);
+        }
+    }
+}
+
 template <int R, int W, int SW, bool STRIDED, typename T>
 __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorMap* map, long long tile,
                                            cplx<T>* buf, unsigned long long* bar, int lane) {
@@ -364,28 +392,9 @@ __device__ __forceinline__ void stage_tile(const PassArgs<T>& a, const CUtensorM
             tma_load_3d(buf, map, (int)(2 * g.first), 0, (int)(p * (R / a.rb)), bar);
         }
     } else if (STRIDED) {
-        const V* src = a.src + g.base;
-        if constexpr (sizeof(V) == 16) {
-            const unsigned rb = (unsigned)(g.nvalid * sizeof(V));
-            if (lane == 0) mbar_expect_tx(bar, rb * R);
-            __syncwarp();
-            for (int j = lane; j < R; j += 32) tma_load_1d(buf + j * SW, src + (long long)j * a.C, rb, bar);
-        } else {
-            // total bytes: sum over rows of round16(shift_j*8 + nvalid*8)
-            const long long b0 = g.base & 1;
-            const unsigned odd = (unsigned)(a.C & 1);
-            const unsigned n8 = (unsigned)g.nvalid * 8u;
-            const unsigned sz0 = (n8 + 15u) & ~15u;              // shift 0
-            const unsigned sz1 = (n8 + 8u + 15u) & ~15u;         // shift 1
-            const unsigned rows_shift1 = odd ? (unsigned)(b0 ? (R + 1) / 2 : R / 2) : (unsigned)(b0 ? R : 0);
-            if (lane == 0) mbar_expect_tx(bar, rows_shift1 * sz1 + ((unsigned)R - rows_shift1) * sz0);
-            __syncwarp();
-            for (int j = lane; j < R; j += 32) {
-                const unsigned sh = (unsigned)(b0 ^ (j & odd));
-                const V* row = src + (long long)j * a.C - sh;
-                tma_load_1d(buf + j * SW, row, sh ? sz1 : sz0, bar);
-            }
-        }
+        // one bulk copy per row (tiles a tensor map cannot describe): out of
+        // line, fp64 tiles always take the tensor-map path
+        stage_rows<R, W, SW>(a, g, buf, bar, lane);
     } else if (a.swz) {
         if (lane == 0) {
             mbar_expect_tx(bar, (unsigned)(R * W * sizeof(V)));
