@@ -497,6 +497,64 @@ __device__ __noinline__ cplx<T> dit_epilogue(const PassArgs<T>& a, cplx<T> y, lo
     return y;
 }
 
+// Warp-local DIF scatter.  The last DIF step writes group g's outputs into the
+// input block of g' = digitwise rev(g) (an involution on the last step's
+// groups), so a thread map under which every warp's groups are closed under
+// g -> g' lets the scatter synchronise with __syncwarp instead of a CTA
+// barrier.  ScatterMap packs the orbits (pairs and fixed points) into blocks of
+// GPW groups (the groups one warp holds); ok = false when they do not pack.
+#ifndef PAFFT_WARP_SCATTER
+#define PAFFT_WARP_SCATTER 1
+#endif
+template <typename FA, int RADIX, int GPW> struct ScatterMap {
+    static constexpr int NG = FA::G(FA::NS - 1);
+    int sigma[NG];
+    bool ok;
+    constexpr ScatterMap() : sigma{}, ok(true) {
+        int partner[NG] = {};
+        for (int g = 0; g < NG; ++g) {
+            int hi = g, rv = 0, w = 1;
+            for (int jj = FA::NS - 2; jj >= 0; --jj) {  // least significant digit first
+                const int fj = FA::f(jj), d = hi % fj;
+                hi /= fj;
+                rv += revd_rt(d, fj) * w;
+                w *= fj;
+            }
+            partner[g] = rv;
+        }
+        bool used[NG] = {};
+        int pos = 0;
+        while (pos < NG && ok) {
+            const int room = GPW - pos % GPW;
+            int pick = -1;
+            for (int g = 0; g < NG && pick < 0; ++g)
+                if (!used[g] && partner[g] != g && room >= 2) pick = g;
+            if (pick < 0)
+                for (int g = 0; g < NG && pick < 0; ++g)
+                    if (!used[g] && partner[g] == g) pick = g;
+            if (pick < 0) {
+                ok = false;
+                break;
+            }
+            used[pick] = true;
+            sigma[pos++] = pick;
+            if (partner[pick] != pick) {
+                used[partner[pick]] = true;
+                sigma[pos++] = partner[pick];
+            }
+        }
+    }
+    static constexpr int revd_rt(int k, int P) {
+        int o = 0;
+        for (int p = 1; p < P; p *= RADIX) {
+            o = o * RADIX + k % RADIX;
+            k /= RADIX;
+        }
+        return o;
+    }
+};
+template <typename FA, int RADIX, int GPW> __constant__ ScatterMap<FA, RADIX, GPW> kScatter{};
+
 // One tile of a pass (the tile is staged in `buf`; the caller waited for it):
 // the column transforms, the epilogue, and the issue of the tile's bulk/tensor
 // store (committed as one bulk group by warp 0 lane 0).  `service` is called by
@@ -519,6 +577,11 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     // fp32 strided tiles (per-row shifted layout) keep register stores.
     constexpr bool TSTORE = !SHIFT;
     constexpr int NGL = FA::G(NS - 1) / GMIN;  // last-step groups per thread
+    // warp-local DIF scatter (ScatterMap): strided DIF, one last-step group per
+    // thread, whole warps of W-column groups
+    constexpr int GPWS = (STRIDED && W <= 32) ? 32 / W : 1;  // groups per warp
+    constexpr bool WSCAT = PAFFT_WARP_SCATTER && KIND == KIND_DIF && STRIDED && !SHIFT && NGL == 1 && NS >= 2 &&
+                           W <= 32 && 32 % W == 0 && ScatterMap<FA, RADIX, GPWS>().ok;
     // Chebyshev twiddle powers for 16-point steps (codelets.cuh) where enough
     // warps hide its longer chain: contiguous tiles of >= 256 threads
     constexpr bool CHEB16 = !STRIDED && Pol::NT >= 256;
@@ -617,7 +680,8 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
 #pragma unroll
             for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
                 constexpr bool SQ = SmallQ<FA, I>::on;
-                const int g = SQ ? (gt % (FA::G(I) / QI)) * QI + gt / (FA::G(I) / QI) : gt + j * GMIN;
+                int g = SQ ? (gt % (FA::G(I) / QI)) * QI + gt / (FA::G(I) / QI) : gt + j * GMIN;
+                if constexpr (WSCAT && I == NS - 1) g = kScatter<FA, RADIX, GPWS>.sigma[gt];
                 const int hi = g / QI, lo = g - (g / QI) * QI;
                 const int sb = hi * PI + lo;
                 V z[FI];
@@ -682,7 +746,8 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
 
     if constexpr (KIND == KIND_DIF) {
         if constexpr (TSTORE) {
-            __syncthreads();
+            if constexpr (WSCAT) __syncwarp();
+            else __syncthreads();
 #pragma unroll
             for (int j = 0; j < (act ? NGL : 0); ++j)
 #pragma unroll
