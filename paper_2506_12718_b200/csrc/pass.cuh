@@ -56,6 +56,9 @@
 #ifndef PAFFT_HOIST_FMAX
 #define PAFFT_HOIST_FMAX 9
 #endif
+#ifndef PAFFT_OK_CT
+#define PAFFT_OK_CT 1
+#endif
 #ifndef PAFFT_GHAT_PF
 #define PAFFT_GHAT_PF 1
 #endif
@@ -600,7 +603,9 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     // CONV: this column's filter block (the panel's position inside its signal)
     const V* const gblk =
         KIND == KIND_CONV ? a.ghat + (long long)((unsigned)(first + c) % (unsigned)(a.N / R)) * R : nullptr;
-    const bool ok = act && c < geo.nvalid;
+    // one-block double-buffered contiguous tiles are always full: ok is the
+    // activity flag (PAFFT_OK_CT)
+    const bool ok = (PAFFT_OK_CT && !STRIDED && W == 1 && Pol::NBUF == 2) ? act : (act && c < geo.nvalid);
     V* const scol = STRIDED ? buf + c : buf + c * R;
     // shared element of tile row `row` for this thread's column
     const int codd = SHIFT && !a.use_tmap ? (a.C & 1) : 0;
