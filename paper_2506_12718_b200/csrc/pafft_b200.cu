@@ -408,12 +408,17 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
         // 2-D tensor map staging needs 16-byte row strides (always for fp64,
         // even C for fp32); otherwise one bulk copy per row.
         d.sw = p->esize == 8 ? d.W + 2 : d.W;
-        d.use_tmap = (p->esize == 16 || (d.C % 2) == 0) && env_int("PAFFT_NO_TMAP", 0) == 0;
+        // fp64 strided tiles always stage and store through tensor maps (their
+        // tile store is a tensor store); fp32 ones may use per-row copies
+        d.use_tmap = p->esize == 16 || ((d.C % 2) == 0 && env_int("PAFFT_NO_TMAP", 0) == 0);
         int rb = 1;
         for (int v = 1; v <= 256 && v <= d.R; ++v)
             if (d.R % v == 0) rb = v;
         d.rb = rb;
-        if (d.R / rb > 256) d.use_tmap = 0;
+        if (d.R / rb > 256) {
+            if (p->esize == 16) return fail(PAFFT_INVALID_ARGUMENT, "strided tile of %d rows has no tensor-map box", d.R);
+            d.use_tmap = 0;
+        }
     }
     d.ext = d.L > 1;
     if (d.ext) ST_TRY(ext_table(p, d.K0, d));
