@@ -48,11 +48,16 @@
 #ifndef PAFFT_SB
 #define PAFFT_SB 1
 #endif
+// Tuning switches (defaults = measured best on B200; DESIGN.md §3 has the A/B
+// numbers).  PAFFT_EXT_HOIST: DIT passes load the first step's external
+// twiddles before waiting for the tile, for codelets of <= PAFFT_HOIST_FMAX
+// points (config 1's 16-point DIT measured 0.5% faster without it).
+// PAFFT_OK_CT: one-block double-buffered contiguous tiles skip the
+// column-in-range test (always full).  PAFFT_GHAT_PF: L2 prefetch of the next
+// CONV tile's filter blocks.
 #ifndef PAFFT_EXT_HOIST
 #define PAFFT_EXT_HOIST 1
 #endif
-// DIT ext hoisting only for codelets of <= 9 points (config 1's 16-point DIT
-// measured 0.5% faster without it)
 #ifndef PAFFT_HOIST_FMAX
 #define PAFFT_HOIST_FMAX 9
 #endif
