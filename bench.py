@@ -8,16 +8,26 @@ One "step" = one pass of the hot path (pafft::convolve_permfree,
 convolution.cpp:45-52) over one batch of the BASELINE.json configuration:
 config 2 by default (BASELINE configs[1]: n = 3^13, radix 3, batch 64, fp64).
 Inputs are seeded synthetic data with BASELINE's distributions (workload.py).
-Multi-GPU: one process per GPU (torchrun), batch shards with a fixed batch
-per GPU (weak scaling), the prepared filter is broadcast once over NCCL,
-no per-step communication; time = max over ranks of CUDA-event time.
+
+Multi-GPU: one process per GPU (torchrun).  The config's FIXED
+global batch is split into contiguous slices, batch / G per rank (strong
+scaling; `--weak` keeps a fixed per-GPU batch instead); config 1's 100-call
+sequence runs as replicas.  The prepared filter is broadcast once over NCCL,
+there is no per-step communication; time = max over ranks of CUDA-event time.
 
 Prints ONE JSON line (rank 0).  `value` is device-resident throughput
 (inputs in HBM before timing, out-of-place so every step reads fresh inputs
 larger than L2); `e2e` is the same metric through the host-buffer C-ABI call
 (pinned H2D + conv + D2H inside the timed region); `roofline` is the dominant
 kernel against the measured HBM peak; `cpu_baseline` is the reference CPU path
-on this host's cores (oracle/_ref for radix 2/4/8, the oracle port for 3/5).
+on this host's cores (oracle/_ref = pafft itself for radix 2/4/8, the
+pafft-style port for 3/5), 1 warm-up + 3 timed repetitions, median.  With the
+default config the line also carries `configs`: the same measurement for
+every other BASELINE config (1, 3, 4, 5 fp64, 5 fp32) at fewer steps.
+
+The reference arm (`--impl reference`) never imports the product package: its
+inputs come from the oracle's SplitMix64 generator (byte-identical to the
+product's, tests/test_abi.py), and it times the FULL config batch per step.
 """
 from __future__ import annotations
 
@@ -34,6 +44,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 KIND_NAMES = {0: "dif", 1: "dit_fwd", 2: "dit_conj", 3: "conv_mid"}
+SUB_CONFIGS = [(1, "f64"), (3, "f64"), (4, "f64"), (5, "f64"), (5, "f32")]
+# measured FP peaks (tools/probes/peaks.cu, profiles/r01_peaks_probe.log): DFMA / FFMA TFLOP/s
+FP_PEAK = {"f64": 34.08, "f32": 72.06}
 
 
 def parse():
@@ -44,13 +57,50 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch override (0 = config batch)")
+    ap.add_argument("--batch", type=int, default=0, help="global batch override (0 = config batch)")
+    ap.add_argument("--weak", action="store_true", help="fixed per-GPU batch (weak scaling) instead of a split")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the per-config sub-results")
+    ap.add_argument("--sub-steps", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--graph", type=int, default=-1,
                     help="capture a step in a CUDA graph (default: on for multi-call steps, config 1)")
     return ap.parse_args()
+
+
+def workload_mod():
+    """workload.py loaded by path as a standalone module: importing it through
+    the package would run paper_2506_12718_b200/__init__.py, which maps the
+    product library -- the reference arm must never do that."""
+    mod = sys.modules.get("_pafft_workload")
+    if mod is None:
+        import importlib.util
+        spec = importlib.util.spec_from_file_location(
+            "_pafft_workload", os.path.join(ROOT, "paper_2506_12718_b200", "workload.py"))
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules["_pafft_workload"] = mod
+        spec.loader.exec_module(mod)
+    return mod
+
+
+def repo_libs_loaded():
+    """Shared objects under the repo this process has mapped (/proc/self/maps):
+    the reference arm must show only oracle/*, the GPU arm the product library."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                path = line.split()[-1] if len(line.split()) >= 6 else ""
+                if path.endswith(".so") and os.path.realpath(path).startswith(os.path.realpath(ROOT)):
+                    libs.add(os.path.relpath(os.path.realpath(path), os.path.realpath(ROOT)))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
+def cfg_key(idx, prec):
+    return f"config{idx}" + ("" if prec == "f64" else "_" + prec)
 
 
 # ------------------------------------------------------------------ clocks
@@ -120,8 +170,8 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(key):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+def ncu_info(key):
+    """Per-launch figures of a config's dominant kernel from the committed ncu summary."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             return json.load(f).get(key)
@@ -130,47 +180,6 @@ def ncu_traffic(key):
 
 
 # ------------------------------------------------------------- CPU baseline
-def cpu_comparator(cfg, count, threads):
-    """Returns (run() -> seconds for `count` convs, kind, sample_desc).  TEST/BASELINE
-    leg only: this is the one place bench.py executes oracle/ (as the timed CPU
-    comparator, never as the measured product)."""
-    import numpy as np
-    import oracle
-    from paper_2506_12718_b200 import workload
-
-    h = workload.impulse(cfg)
-    xs = workload.signals(cfg, 0, count)
-    if cfg.radix in (2, 4, 8) and oracle.Ref.available():
-        R = oracle.Ref()
-        rp = R.plan(cfg.radix, cfg.dims)
-        ghat = rp.prepare_filter(rp.filter_from_impulse(h))
-        batch = rp.batch(ghat, xs)
-        return (lambda: batch.run(threads)), "reference", \
-            f"pafft::convolve_permfree (reference library built from its sources), {count} signals of the workload"
-    O = oracle.Oracle()
-    op = O.plan(cfg.radix, cfg.dims)
-    ghat = op.prepare_filter(op.filter_from_impulse(h))
-    gr, gi = np.ascontiguousarray(ghat.real), np.ascontiguousarray(ghat.imag)
-    re0, im0 = np.ascontiguousarray(xs.real), np.ascontiguousarray(xs.imag)
-    # radix 3/5 (not representable in pafft, core.hpp:14-19): pafft's ladder
-    # loop nest with a hand-expanded radix-r combine (oracle/fast_ladders.c);
-    # its radix-2 instance runs at pafft's own speed (tools/port_calibration.py)
-    fast = len(cfg.dims) == 1 and cfg.radix in (2, 3, 4, 5)
-    conv = op.convolve_permfree_fast_batch_split if fast else op.convolve_permfree_batch_split
-
-    def run():
-        re, im = re0.copy(), im0.copy()
-        t = time.perf_counter()
-        conv(gr, gi, re, im, count, threads)
-        return time.perf_counter() - t
-
-    what = ("pafft's ladder loop nest with a hand-expanded radix-%d combine (oracle/fast_ladders.c; its radix-2 "
-            "instance matches pafft's own speed, tools/port_calibration.py)" % cfg.radix) if fast else \
-        "oracle restatement of pafft's ladders"
-    return run, "port", f"{what}; radix {cfg.radix} is not representable in pafft (core.hpp:14-19); " \
-                        f"{count} signals of the workload"
-
-
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -178,64 +187,196 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def cpu_sample_count(cfg, threads):
-    # bounded: ~10-30 s of CPU work at ~20 ns per point-stage per core
-    work_per_conv = cfg.total * sum(cfg.stages) * 2 * 2e-8  # seconds per conv per core, rough
-    count = max(threads, int(round(20.0 / max(work_per_conv, 1e-6))))
-    return max(1, min(count, threads * 4, cfg.batch * cfg.calls))
+class CpuComparator:
+    """The reference CPU path on this host (TEST/BASELINE leg only: the one place
+    bench.py executes oracle/, as the timed comparator, never as the product).
+    radix 2/4/8: pafft::convolve_permfree itself (oracle/_ref, compiled from the
+    reference's sources); radix 3/5 (not representable in pafft, core.hpp:14-19):
+    pafft's ladder loop nest with a hand-expanded radix-r combine
+    (oracle/fast_ladders.c; its radix-2 instance runs at pafft's own speed,
+    profiles/r01_cpu_port_calibration.log).  Inputs from the oracle's SplitMix64
+    (identical bytes to the product generator); this process never maps the
+    product library."""
+
+    def __init__(self, cfg, count):
+        import numpy as np
+        import oracle
+        workload = workload_mod()
+
+        self.cfg, self.count = cfg, count
+        O = oracle.Oracle()
+        h = workload.impulse(cfg, fill_normal=O.fill_normal)
+        seeds = [workload.seed_signal(b) for b in range(count)]
+        self.re0, self.im0 = O.fill_signals_split(cfg.signal == "uniform", seeds, cfg.total)
+        self.ref = cfg.radix in (2, 4, 8) and oracle.Ref.available()
+        if self.ref:
+            R = oracle.Ref()
+            self.rp = R.plan(cfg.radix, cfg.dims)
+            self.ghat = self.rp.prepare_filter(self.rp.filter_from_impulse(h))
+            self.kind = "reference"
+            self.what = "pafft::convolve_permfree (the reference library built from its own sources, oracle/_ref)"
+        else:
+            op = O.plan(cfg.radix, cfg.dims)
+            self.op = op
+            ghat = op.prepare_filter(op.filter_from_impulse(h))
+            self.gr, self.gi = np.ascontiguousarray(ghat.real), np.ascontiguousarray(ghat.imag)
+            fast = len(cfg.dims) == 1 and cfg.radix in (2, 3, 4, 5)
+            self.conv = op.convolve_permfree_fast_batch_split if fast else op.convolve_permfree_batch_split
+            self.kind = "port"
+            self.what = (f"pafft's ladder loop nest with a hand-expanded radix-{cfg.radix} combine "
+                         "(oracle/fast_ladders.c); radix %d is not representable in pafft (core.hpp:14-19)"
+                         % cfg.radix) if fast else "oracle restatement of pafft's ladders"
+
+    def run(self, threads, count=None):
+        """Seconds for one batch of `count` convolutions (inputs re-staged
+        outside the timed region, so every repetition convolves fresh signals)."""
+        n = count or self.count
+        if self.ref:
+            batch = self.rp.batch_split(self.ghat, self.re0[:n], self.im0[:n])
+            return batch.run(threads)
+        re, im = self.re0[:n].copy(), self.im0[:n].copy()
+        t = time.perf_counter()
+        self.conv(self.gr, self.gi, re, im, n, threads)
+        return time.perf_counter() - t
 
 
-def run_reference(args, cfg, rank):
+def pinned_one_core(fn):
+    """Run fn() with this thread (and the threads it spawns) pinned to one core,
+    pafft's methodology (bench.cpp:52-59)."""
+    try:
+        old = os.sched_getaffinity(0)
+    except AttributeError:
+        return fn(), None
+    core = min(old)
+    os.sched_setaffinity(0, {core})
+    try:
+        return fn(), core
+    finally:
+        os.sched_setaffinity(0, old)
+
+
+def cpu_measure(cfg, count, reps=3, warmup=1, one_core=True):
+    """1 warm-up, >= 3 repetitions, median; all host cores sharing
+    one plan/filter over the batch, plus one pinned core."""
+    threads = cpu_threads()
+    comp = CpuComparator(cfg, count)
+    for _ in range(warmup):
+        comp.run(threads)
+    secs = [comp.run(threads) for _ in range(reps)]
+    med = statistics.median(secs)
+    out = {"value": count / med, "unit": "conv/s", "cores": threads, "kind": comp.kind,
+           "sample": f"{comp.what}; {count} signals of the workload per repetition, {threads} threads sharing one "
+                     f"plan and prepared filter; {warmup} warm-up + {reps} repetitions, median",
+           "reps_s": secs}
+    if one_core:
+        def one():
+            comp.run(1, 1)
+            return statistics.median([comp.run(1, 1) for _ in range(reps)])
+        s1, core = pinned_one_core(one)
+        out["value_1core"] = 1.0 / s1
+        out["one_core"] = f"1 signal per repetition, pinned to cpu {core}, {warmup} warm-up + {reps} reps, median"
+    return out
+
+
+def run_reference(args, rank):
+    """`--impl reference`: the reference CPU path on all host cores, the full
+    config batch per step (rank 0 only; other ranks exit without work)."""
     if rank != 0:
         return
-    threads = cpu_threads()
-    count = cpu_sample_count(cfg, threads)
-    run, kind, sample = cpu_comparator(cfg, count, threads)
-    for _ in range(min(args.warmup, 1)):
-        run()
-    secs = [run() for _ in range(args.steps)]
+    workload = workload_mod()
+
+    def measure(cfg, steps, warmup):
+        count = cfg.calls if cfg.calls > 1 else cfg.batch
+        comp = CpuComparator(cfg, count)
+        threads = cpu_threads()
+        for _ in range(warmup):
+            comp.run(threads)
+        secs = [comp.run(threads) for _ in range(steps)]
+        return comp, threads, count, secs
+
+    cfg = workload.get_config(args.config, "f64")
+    comp, threads, count, secs = measure(cfg, args.steps, args.warmup)
     total = sum(secs)
     value = count * len(secs) / total
     line = {
         "impl": "reference", "metric": "convolutions_per_second", "value": value, "unit": "conv/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(secs), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / len(secs), "higher_is_better": True,
+        "scaling": "weak" if cfg.calls > 1 or args.weak else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, BASELINE distributions)",
         "config": {"workload": f"config{cfg.idx}: {cfg.note}", "radix": cfg.radix, "dims": cfg.dims,
-                   "batch_per_step": count, "precision": "f64"},
-        "cpu_baseline": {"value": value, "unit": "conv/s", "cores": threads, "kind": kind, "sample": sample},
+                   "global_batch": count, "batch_per_step": count, "precision": "f64"},
+        "cpu_baseline": {"value": value, "unit": "conv/s", "cores": threads, "kind": comp.kind,
+                         "sample": f"{comp.what}; the full batch of {count} signals per step, {threads} threads"},
         "e2e": {"value": value, "unit": "conv/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_s": {"median": statistics.median(secs), "min": min(secs), "max": max(secs)},
     }
+    if not args.no_sub and args.config == 2:
+        subs = {}
+        for idx, prec in SUB_CONFIGS:
+            if prec != "f64":
+                subs[cfg_key(idx, prec)] = {"same_as": cfg_key(idx, "f64"),
+                                            "note": "no fp32 CPU path: the fp32 GPU result is checked against the "
+                                                    "fp64 pipeline on rounded inputs (BASELINE.md 4)"}
+                continue
+            c = workload.get_config(idx, "f64")
+            k = max(3, min(args.sub_steps, 3))
+            comp, threads, count, secs = measure(c, k, 1)
+            med = statistics.median(secs)
+            subs[cfg_key(idx, prec)] = {"value": count / med, "unit": "conv/s", "cores": threads, "kind": comp.kind,
+                                        "batch_per_step": count, "steps": k, "warmup": 1,
+                                        "step_s_median": med, "workload": f"config{idx}: {c.note}"}
+            del comp
+        line["configs"] = subs
+    line["repo_libs_loaded"] = repo_libs_loaded()
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------- GPU arm
-def main():
-    args = parse()
-    from paper_2506_12718_b200 import workload
+class Gpu:
+    """Per-process GPU context (device, rank, world, process group)."""
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = workload.get_config(args.config, args.precision)
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
 
-    if args.impl == "reference":
-        run_reference(args, workload.get_config(args.config, "f64"), rank)
-        return
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        self.dev = torch.device("cuda", self.local)
+        self.gpu_index = self.local
+        cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if cvd:
+            try:
+                self.gpu_index = int(cvd.split(",")[self.local])
+            except ValueError:
+                pass
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+
+def gpu_measure(g, cfg, args, steps, warmup, with_e2e, with_cpu):
+    """One BASELINE config through the product path on this rank's shard."""
+    import ctypes as C
 
     import numpy as np
     import torch
-    import torch.distributed as dist
-    import paper_2506_12718_b200 as pf
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+    import paper_2506_12718_b200 as pf
+    from paper_2506_12718_b200 import dist as pdist
+    from paper_2506_12718_b200 import workload
+
+    world, rank, dev = g.world, g.rank, g.dev
     prec = pf.F64 if cfg.precision == "f64" else pf.F32
     cdt = torch.complex128 if prec == pf.F64 else torch.complex64
     ndt = np.complex128 if prec == pf.F64 else np.complex64
-    plan = pf.Plan(cfg.radix, cfg.dims, precision=prec, device=local)
+    plan = pf.Plan(cfg.radix, cfg.dims, precision=prec, device=g.local)
     N = cfg.total
     S = workload.signal_bytes(cfg)
 
@@ -248,42 +389,50 @@ def main():
     else:
         filt = pf.empty_filter(plan)
     if world > 1:
-        from paper_2506_12718_b200 import dist as pdist
         pdist.broadcast_filter_tensors([pf.filter_device_tensor(filt), pf.filter_device_tensor(filt, scaled=True)])
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t_prep
 
-    # ---- inputs: per-rank shard (fixed per-GPU batch), resident in HBM
-    from paper_2506_12718_b200 import dist as pdist
-    per = args.batch or (cfg.calls if cfg.calls > 1 else cfg.batch)
-    first, per = pdist.shard(per, rank)
-    host = torch.empty((per, N), dtype=cdt, pin_memory=True)
-    hv = host.numpy()
-    if prec == pf.F64:
-        workload.signals(cfg, first, per, out=hv)
+    # ---- inputs: this rank's slice of the global batch, resident in HBM
+    calls = cfg.calls if cfg.calls > 1 else 1
+    weak = args.weak or calls > 1  # config 1 (the call sequence) runs as replicas
+    if calls > 1:
+        first, per = 0, calls
+        global_batch = calls * world
+    elif weak:
+        per_rank = args.batch or cfg.batch
+        first, per = pdist.shard_weak(per_rank, rank)
+        global_batch = per_rank * world
     else:
-        hv[:] = workload.signals(cfg, first, per).astype(np.complex64)
+        global_batch = args.batch or cfg.batch
+        first, per = pdist.shard(global_batch, world, rank)
+    host = torch.empty((max(per, 1), N), dtype=cdt, pin_memory=True)
+    hv = host.numpy()
+    if per:
+        if prec == pf.F64:
+            workload.signals(cfg, first, per, out=hv)
+        else:
+            for c0 in range(0, per, 256):
+                c1 = min(per, c0 + 256)
+                hv[c0:c1] = workload.signals(cfg, first + c0, c1 - c0).astype(np.complex64)
     x = host.to(dev)
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
 
     npass = plan.num_passes()
     infos = []
-    import ctypes as C
     for i in range(npass):
         k, a, R, s = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         pf._check(pf.lib.pafft_plan_pass_info(plan._h, i, C.byref(k), C.byref(a), C.byref(R), C.byref(s)))
         infos.append({"kind": KIND_NAMES[k.value], "axis": a.value, "R": R.value, "stages": s.value})
 
-    calls = cfg.calls if cfg.calls > 1 else 1
     bpc = per // calls  # signals per call
-    sptr = C.c_void_p(stream.cuda_stream)
-    chunk = int(pf.lib.pafft_plan_chunk_signals(plan._h)) or bpc
-    chunk = max(1, min(chunk, bpc))
+    sptr = [C.c_void_p(stream.cuda_stream)]
     esz = x.element_size()
 
     def launch_pass(i, xs, ys, nb):
-        pf._check(pf.lib.pafft_convolve_permfree_pass(plan._h, filt._h, C.c_void_p(xs), C.c_void_p(ys), nb, i, sptr))
+        pf._check(pf.lib.pafft_convolve_permfree_pass(plan._h, filt._h, C.c_void_p(xs), C.c_void_p(ys), nb, i,
+                                                      sptr[0]))
 
     def step():
         # the public hot-path call: convolve_permfree out of place, per call
@@ -291,64 +440,51 @@ def main():
             xs = x.data_ptr() + c * bpc * N * esz
             ys = y.data_ptr() + c * bpc * N * esz
             pf._check(pf.lib.pafft_convolve_permfree_oop(plan._h, filt._h, C.c_void_p(xs), C.c_void_p(ys), bpc,
-                                                         sptr))
+                                                         sptr[0]))
 
-    gpu_index = local
-    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
-    if cvd:
-        try:
-            gpu_index = int(cvd.split(",")[local])
-        except ValueError:
-            pass
-    sampler = ClockSampler(gpu_index)
+    sampler = ClockSampler(g.gpu_index)
     sampler.start()
-
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     # launch-bound multi-call steps (config 1: 100 batch-1 calls) replay a
     # captured CUDA graph of the same calls instead of re-launching from Python
     use_graph = args.graph if args.graph >= 0 else int(calls > 1)
     graph_launches = 0
-    if use_graph:
-        g = torch.cuda.CUDAGraph()
+    if use_graph and per:
+        gr = torch.cuda.CUDAGraph()
         cs = torch.cuda.Stream()
         cs.wait_stream(stream)
         l0 = pf.kernel_launch_count()
         with torch.cuda.stream(cs):
-            sptr_saved = sptr
-            sptr = C.c_void_p(cs.cuda_stream)
-            with torch.cuda.graph(g, stream=cs):
+            saved = sptr[0]
+            sptr[0] = C.c_void_p(cs.cuda_stream)
+            with torch.cuda.graph(gr, stream=cs):
                 step()
-            sptr = sptr_saved
+            sptr[0] = saved
         graph_launches = pf.kernel_launch_count() - l0
         stream.wait_stream(cs)
-        plain_step = step
 
         def step():  # noqa: F811
-            g.replay()
+            gr.replay()
 
         step()
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    g.barrier()
 
     # ---- timed region (device-resident, CUDA events, max over ranks)
     launches0 = pf.kernel_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    g.barrier()
     tw0 = time.time()
     e0.record(stream)
-    for k in range(args.steps):
+    for _ in range(steps):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
-    tw1 = time.time()
-    if world > 1:
-        dist.barrier()
-    launches = pf.kernel_launch_count() - launches0 + graph_launches * args.steps
+    g.barrier()
+    launches = pf.kernel_launch_count() - launches0 + graph_launches * steps
     ms_max = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
     # keep the GPU busy (untimed) until the clock sampler has >= 1 s of samples
     t_soak = time.time()
@@ -359,39 +495,40 @@ def main():
     sampler.stop()
     clocks = sampler.summary(tw0 - 0.05, tw_end + 0.05)
 
-    # ---- per-pass device time: the same launches the pipeline issues (one
-    # L2 chunk per launch), run one at a time on one stream between CUDA events
-    reps = max(1, min(args.steps, 8))
-    nch = max(1, bpc // chunk)
-    pev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(npass)]
-           for _ in range(reps * nch)]
-    for r in range(reps):
-        for q in range(nch):
-            xs = x.data_ptr() + q * chunk * N * esz
-            ys = y.data_ptr() + q * chunk * N * esz
+    # ---- per-pass device time: the same launches one call issues, one at a
+    # time on one stream between CUDA events
+    reps = max(1, min(steps, 8))
+    pass_ms = [0.0] * npass
+    if bpc:
+        pev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(npass)]
+               for _ in range(reps)]
+        for r in range(reps):
             for i in range(npass):
-                ev = pev[r * nch + q][i]
+                ev = pev[r][i]
                 ev[0].record(stream)
-                launch_pass(i, xs, ys, chunk)
+                launch_pass(i, x.data_ptr(), y.data_ptr(), bpc)
                 ev[1].record(stream)
-    torch.cuda.synchronize()
-    pass_ms = [statistics.mean(ev[i][0].elapsed_time(ev[i][1]) for ev in pev) for i in range(npass)]
+        torch.cuda.synchronize()
+        pass_ms = [statistics.mean(ev[i][0].elapsed_time(ev[i][1]) for ev in pev) for i in range(npass)]
     dom = max(range(npass), key=lambda i: pass_ms[i])
-    dom_bytes = 2.0 * S * chunk + (S if infos[dom]["kind"] == "conv_mid" else 0.0)
+    dom_bytes = 2.0 * S * bpc + (S if infos[dom]["kind"] == "conv_mid" else 0.0)
     peak, peak_src = measured_peak()
-    achieved = dom_bytes / (pass_ms[dom] * 1e-3) / 1e9
+    achieved = dom_bytes / (pass_ms[dom] * 1e-3) / 1e9 if pass_ms[dom] > 0 else 0.0
 
-    convs = per * world * args.steps
+    convs = global_batch * steps
     value = convs / (ms_max * 1e-3)
-    conv_gbs = value / world * workload.bytes_per_conv(cfg, world) / 1e9
+    bpc_alg = workload.bytes_per_conv(cfg, world, weak)
+    conv_gbs = value / world * bpc_alg / 1e9
     flops = workload.flops_per_conv(cfg)
-    fp_peak = 34.08 if cfg.precision == "f64" else 72.06  # DFMA / FFMA TFLOP/s, measured
+    fp_peak = FP_PEAK[cfg.precision]
+    key = cfg_key(cfg.idx, cfg.precision)
+    ncu = ncu_info(key) or {}
 
     # ---- e2e: host buffers through the C-ABI (pinned H2D + conv + D2H timed)
     e2e = None
-    if not args.no_e2e:
+    if with_e2e:
         yh = torch.empty_like(host, pin_memory=True)
-        ysteps = args.e2e_steps or max(2, min(args.steps, 5))
+        ysteps = args.e2e_steps or max(2, min(steps, 5))
         xv, yv = host.numpy(), yh.numpy()
 
         def host_step():
@@ -402,76 +539,114 @@ def main():
                                                                   C.c_void_p(ys.ctypes.data), bpc))
 
         host_step()
-        if world > 1:
-            dist.barrier()
+        g.barrier()
         t = time.perf_counter()
         for _ in range(ysteps):
             host_step()
         et = pdist.max_over_ranks(time.perf_counter() - t, dev)
-        e2e = {"value": per * world * ysteps / et, "unit": "conv/s", "h2d_bytes_per_step": per * S,
-               "d2h_bytes_per_step": per * S, "steps": ysteps, "pipelined": "3 streams, 64 MiB chunks, pinned"}
+        e2e = {"value": global_batch * ysteps / et, "unit": "conv/s", "h2d_bytes_per_step": per * S,
+               "d2h_bytes_per_step": per * S, "steps": ysteps,
+               "pipelined": "3 streams, 64 MiB chunks, pinned host buffers"}
+        del yh
 
-    # ---- CPU baseline (rank 0, N = 1 only)
+    # ---- CPU baseline (rank 0, N = 1 only): bounded sample, median of reps
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if with_cpu and rank == 0 and world == 1:
         try:
-            c64 = workload.get_config(args.config, "f64")
-            threads = cpu_threads()
-            count = cpu_sample_count(c64, threads)
-            run, kind, sample = cpu_comparator(c64, count, threads)
-            secs = run()
-            # one core, pafft's own methodology (bench.cpp:52-59)
-            run1, _, _ = cpu_comparator(c64, 1, 1)
-            secs1 = run1()
-            cpu = {"value": count / secs, "unit": "conv/s", "cores": threads, "kind": kind,
-                   "sample": sample + f"; {threads} threads, one timed batch of {count}",
-                   "value_1core": 1.0 / secs1}
+            # the whole config batch (0.5-2 s per repetition on the box's host)
+            c64 = workload.get_config(cfg.idx, "f64")
+            cpu = cpu_measure(c64, c64.calls if c64.calls > 1 else c64.batch)
         except Exception as e:  # report, never substitute
             cpu = {"value": None, "unit": "conv/s", "cores": cpu_threads(), "kind": "unavailable",
                    "sample": f"{type(e).__name__}: {e}"}
 
-    if rank == 0:
+    out = {
+        "value": value, "unit": "conv/s", "ms_per_step": ms_max / steps, "steps": steps, "warmup": warmup,
+        "dtype": cfg.precision,
+        "config": {"workload": f"config{cfg.idx}: {cfg.note}", "radix": cfg.radix, "dims": cfg.dims,
+                   "global_batch": global_batch, "batch_per_gpu": per, "calls_per_step": calls,
+                   "precision": cfg.precision,
+                   "parallelism": (f"replicas x{world}" if calls > 1 else
+                                   f"batch split {global_batch}/{world}" if not weak else f"weak x{world}"),
+                   "cuda_graph": bool(use_graph),
+                   "l2": f"inputs {per * S / 2**30:.2f} GiB per GPU per step > 126 MB L2 (no flush needed)"
+                   if per * S > 2 * 126e6 else "inputs smaller than 2x L2; out-of-place fresh buffer per call"},
+        "scaling": "weak" if weak else "strong",
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu.get("traffic") if isinstance(ncu, dict) else None,
+                     "kernel": f"pass{dom}:{infos[dom]['kind']}(R={infos[dom]['R']})",
+                     "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": pass_ms[dom],
+                     "signals_per_launch": bpc, "peak_source": peak_src,
+                     # what actually limits that kernel (ncu --set full of the same kernel, committed)
+                     "limiter": ncu.get("limiter") if isinstance(ncu, dict) else None},
+        "conv_roofline": {"bytes_per_conv": bpc_alg, "achieved_gbs_per_gpu": conv_gbs,
+                          "frac_of_hbm": conv_gbs / peak, "frac_of_hbm_datasheet_8tbs": conv_gbs / 8000.0,
+                          "flops_per_conv": flops, "achieved_tflops_per_gpu": value / world * flops / 1e12,
+                          "fp_peak_tflops": fp_peak, "frac_of_fp_peak": value / world * flops / 1e12 / fp_peak},
+        "passes": [{**infos[i], "ms": pass_ms[i]} for i in range(npass)],
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+        "prepare_filter_s": t_prep,
+    }
+    del x, y, host, filt, plan
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    from paper_2506_12718_b200 import workload
+
+    g = Gpu(args)
+    cfg = workload.get_config(args.config, args.precision)
+    res = gpu_measure(g, cfg, args, args.steps, args.warmup, not args.no_e2e, not args.no_cpu)
+    subs = None
+    if not args.no_sub and args.config == 2 and args.precision == "f64" and not args.batch:
+        subs = {}
+        for idx, prec in SUB_CONFIGS:
+            c = workload.get_config(idx, prec)
+            k = max(3, args.sub_steps)
+            try:
+                r = gpu_measure(g, c, args, k, 3, not args.no_e2e, False)
+                subs[cfg_key(idx, prec)] = {kk: r[kk] for kk in ("value", "unit", "ms_per_step", "steps", "warmup",
+                                                                 "dtype", "config", "scaling", "roofline",
+                                                                 "conv_roofline", "passes", "e2e", "gpu_launches",
+                                                                 "clocks")}
+            except Exception as e:  # report, never substitute
+                subs[cfg_key(idx, prec)] = {"error": f"{type(e).__name__}: {e}"}
+    if g.rank == 0:
         line = {
             "metric": "convolutions_per_second",
-            "value": value,
+            "value": res["value"],
             "unit": "conv/s",
-            "n_gpus": world,
+            "n_gpus": g.world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": ms_max / args.steps,
+            "ms_per_step": res["ms_per_step"],
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": res["scaling"],
             "vs_baseline": None,
-            "dtype": cfg.precision,
+            "dtype": res["dtype"],
             "data": "synthetic (seeded SplitMix64, BASELINE distributions; inputs device-resident, out of place)",
-            "config": {"workload": f"config{cfg.idx}: {cfg.note}", "radix": cfg.radix, "dims": cfg.dims,
-                       "batch_per_gpu": per, "calls_per_step": calls, "global_batch": per * world,
-                       "precision": cfg.precision, "parallelism": f"batch-sharded x{world}",
-                       "cuda_graph": bool(use_graph),
-                       "l2": f"inputs {per * S / 2**30:.2f} GiB per GPU per step > 126 MB L2 (no flush needed)"
-                       if per * S > 2 * 126e6 else "inputs smaller than 2x L2; out-of-place fresh buffer per call"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(f"config{cfg.idx}_{cfg.precision}"),
-                         "kernel": f"pass{dom}:{infos[dom]['kind']}(R={infos[dom]['R']})",
-                         "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": pass_ms[dom],
-                         "signals_per_launch": chunk,
-                         "peak_source": peak_src,
-                         # what binds it (ncu --set full of the same kernel, committed)
-                         "ncu_pipes": ncu_traffic(f"config{cfg.idx}_{cfg.precision}_pipes")},
-            "conv_roofline": {"bytes_per_conv": workload.bytes_per_conv(cfg, world), "achieved_gbs_per_gpu": conv_gbs,
-                              "frac_of_hbm": conv_gbs / peak, "frac_of_hbm_datasheet_8tbs": conv_gbs / 8000.0,
-                              "flops_per_conv": flops, "achieved_tflops_per_gpu": value / world * flops / 1e12,
-                              # FP peaks measured by tools/probes/peaks.cu (profiles/r01_peaks_probe.log)
-                              "fp_peak_tflops": fp_peak, "frac_of_fp_peak": value / world * flops / 1e12 / fp_peak},
-            "passes": [{**infos[i], "ms": pass_ms[i]} for i in range(npass)],
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clocks,
-            "cpu_baseline": cpu,
-            "prepare_filter_s": t_prep,
+            **{k: res[k] for k in ("config", "roofline", "conv_roofline", "passes", "e2e", "gpu_launches", "clocks",
+                                   "cpu_baseline", "prepare_filter_s")},
         }
+        if subs is not None:
+            line["configs"] = subs
+            line["gpu_launches_all_configs"] = res["gpu_launches"] + sum(
+                s.get("gpu_launches", 0) for s in subs.values())
+        line["repo_libs_loaded"] = repo_libs_loaded()
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if g.world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
 
 

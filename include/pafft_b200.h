@@ -146,14 +146,9 @@ pafft_status pafft_convolve_permfree_oop(pafft_plan_t plan, pafft_filter_t filte
  * passes individually with CUDA events (bench.py roofline). */
 pafft_status pafft_convolve_permfree_pass(pafft_plan_t plan, pafft_filter_t filter, const void* x_dev,
                                           void* y_dev, size_t batch, int i, void* stream);
-/* kind: 0 DIF (A^T group), 1 DIT forward, 2 DIT conjugate, 3 fused middle
+/* kind: 0 DIF (A^T group), 1 DIT forward, 2 DIT conjugate, 3 CONV middle
  * (DIF + x ghat + DIT-conj); axis, R = radix^stages of the pass. */
 pafft_status pafft_plan_pass_info(pafft_plan_t plan, int i, int* kind, int* axis, int* R, int* stages);
-/* Signals per L2-resident chunk when the chunk pipeline is enabled
- * (PAFFT_PIPELINE=1: all passes of one chunk back to back so intermediates
- * stay in L2, two chunks in flight on two internal streams forked from and
- * joined to the caller's stream); 0 = each pass covers the whole batch. */
-size_t pafft_plan_chunk_signals(pafft_plan_t plan);
 /* Drop-in host path: split host arrays (ComplexBuffer), synchronous, H2D and
  * D2H inside.  Mirrors convolve_permfree(ComplexBuffer&, ...) exactly. */
 pafft_status pafft_convolve_permfree_split(pafft_plan_t plan, pafft_filter_t filter, double* re, double* im,

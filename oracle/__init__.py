@@ -137,6 +137,25 @@ class Oracle:
         self.L.orc_fill_normal(seed, n, _p(re), _p(im))
         return re + 1j * im
 
+    def fill_signals_split(self, uniform, seeds, n, threads=None):
+        """Signals seeds[i] -> rows i of (re, im) float64 arrays (SplitMix64,
+        the same bytes as the product generator), generated across threads."""
+        import concurrent.futures as cf
+        count = len(seeds)
+        re, im = np.empty((count, n)), np.empty((count, n))
+        fn = self.L.orc_fill_uniform if uniform else self.L.orc_fill_normal
+
+        def one(i):
+            fn(seeds[i], n, _p(re[i]), _p(im[i]))
+
+        if count <= 1:
+            for i in range(count):
+                one(i)
+        else:
+            with cf.ThreadPoolExecutor(threads or min(count, os.cpu_count() or 4)) as ex:
+                list(ex.map(one, range(count)))
+        return re, im
+
     def pass_count(self):
         return self.L.orc_permutation_pass_count()
 
@@ -337,11 +356,18 @@ class RefPlan:
 
     def batch(self, ghat, signals):
         """Stage `signals` (batch x total complex) for timed batched runs."""
-        gr, gi = _split(ghat)
         s = np.ascontiguousarray(signals, dtype=np.complex128).reshape(-1)
-        sr, si = np.ascontiguousarray(s.real), np.ascontiguousarray(s.imag)
-        n = s.size // self.total
-        h = self.L.ref_batch_create(self.h, _p(gr), _p(gi), _p(sr), _p(si), n)
+        return self.batch_split(ghat, np.ascontiguousarray(s.real), np.ascontiguousarray(s.imag))
+
+    def batch_split(self, ghat, re, im):
+        """Stage split signals (re, im: batch x total float64, C-contiguous)."""
+        gr, gi = _split(ghat)
+        re = np.ascontiguousarray(re, dtype=np.float64)
+        im = np.ascontiguousarray(im, dtype=np.float64)
+        n = re.size // self.total
+        h = self.L.ref_batch_create(self.h, _p(gr), _p(gi), _p(re), _p(im), n)
+        if not h:
+            raise OracleError(-1, "ref_batch_create: " + self.L.ref_last_error().decode())
         return RefBatch(self, h, n)
 
 

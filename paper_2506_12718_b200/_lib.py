@@ -56,7 +56,6 @@ _SIGS = {
     "pafft_convolve_permfree_pass": ([_vp, _vp, _vp, _vp, _sz, C.c_int, _vp], _st),
     "pafft_plan_pass_info": ([_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                               C.POINTER(C.c_int)], _st),
-    "pafft_plan_chunk_signals": ([_vp], _sz),
     "pafft_convolve_permfree_split": ([_vp, _vp, _dp, _dp, _sz], _st),
     "pafft_convolve_permfree_host": ([_vp, _vp, _vp, _sz], _st),
     "pafft_convolve_permfree_host_oop": ([_vp, _vp, _vp, _vp, _sz], _st),

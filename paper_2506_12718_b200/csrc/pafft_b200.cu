@@ -26,7 +26,6 @@
 #include <vector>
 
 #include "../../include/pafft_b200.h"
-#include "fused.cuh"
 #include "pass.cuh"
 #include "registry.h"
 
@@ -80,13 +79,6 @@ Registry& registry() {
         register_r5_f32(reg);
         register_r8_f32(reg);
     });
-    return reg;
-}
-
-FusedRegistry& fused_registry() {
-    static FusedRegistry reg;
-    static std::once_flag once;
-    std::call_once(once, [] { register_fused_f64(reg); });
     return reg;
 }
 
@@ -189,12 +181,14 @@ struct pafft_plan_s {
     std::vector<uint32_t*> rev_dev;            // per-axis digit reversal maps (device)
     std::unique_ptr<DevBuf> stage[4];
     cudaStream_t streams[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaStream_t work[2] = {nullptr, nullptr};  // L2-chunk pipeline streams
-    cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
     std::mutex mu;
     std::mutex host_mu;  // serialises the host-buffer pipeline (plan-owned streams + staging)
     // pass schedules, built once at plan creation (immutable afterwards)
     std::vector<PassDesc> pf, dif, dit_fwd, dit_conj;
+    // slot layout of the filter's kernel copy: the CONV pass's (axis, R,
+    // F0..F3) -- set by the pass schedule, which depends on PAFFT_* tuning
+    // variables read at plan creation, so it is part of the filter key
+    long long layout[6] = {0, 0, 0, 0, 0, 0};
     std::map<std::string, CUtensorMap> tmaps;
 };
 
@@ -205,6 +199,7 @@ struct pafft_filter_s {
     int rank = 0;
     size_t dims[8] = {0};
     int prec = 0, device = 0;
+    long long layout[6] = {0, 0, 0, 0, 0, 0};  // kernel-copy slot layout (plan's CONV pass)
     std::shared_ptr<DevBuf> ghat;         // unscaled, plan precision
     std::shared_ptr<DevBuf> ghat_scaled;  // x (1/N), plan precision (shared by cached filters)
 };
@@ -575,131 +570,6 @@ pafft_status launch(pafft_plan_t p, const PassDesc& d, const void* src, void* ds
                         : launch_t<float>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap);
 }
 
-// ------------------------------------------------ fused convolution --
-// One persistent launch for the three passes of a 1-D permutation-free plan
-// (fused.cuh).  Eligible: exactly DIF (strided) -> CONV -> DIT-conj (strided)
-// with a compiled fused instance for the (radix, R_strided, R_contig) pair.
-const FusedEntry* fused_entry(pafft_plan_t p) {
-    const std::vector<PassDesc>& ps = p->pf;
-    if (ps.size() != 3 || p->prec != 0) return nullptr;
-    if (ps[0].kind != KIND_DIF || ps[1].kind != KIND_CONV || ps[2].kind != KIND_DIT_CONJ) return nullptr;
-    if (ps[0].contig || !ps[1].contig || ps[2].contig || ps[0].R != ps[2].R || !ps[0].use_tmap || !ps[2].use_tmap)
-        return nullptr;
-    for (const auto& e : fused_registry())
-        if (e.prec == p->prec && e.radix == (int)p->radices[ps[0].axis] && e.RD == ps[0].R && e.RC == ps[1].R)
-            return &e;
-    return nullptr;
-}
-
-pafft_status launch_fused(pafft_plan_t p, const FusedEntry& fe, const void* ghat, const void* x, void* y,
-                          size_t batch, cudaStream_t st) {
-    using T = double;
-    const std::vector<PassDesc>& ps = p->pf;
-    FusedArgs<T> fa;
-    memset(&fa, 0, sizeof fa);
-    FusedMaps maps;
-    memset(&maps, 0, sizeof maps);
-    long long total_tiles = 0;
-    for (int i = 0; i < 3; ++i) {
-        PassDesc d = ps[i];
-        d.W = i == 1 ? fe.WC : fe.WD;
-        if (!d.contig) d.sw = d.W;
-        PassArgs<T>& a = fa.p[i];
-        const void* src = i == 0 ? x : (const void*)y;
-        a.src = (const cplx<T>*)src;
-        a.dst = (cplx<T>*)y;
-        const long long per_signal = (long long)p->total / ((long long)d.R * d.C);
-        a.panels = per_signal * (long long)batch;
-        a.panel_elems = (long long)d.R * d.C;
-        a.C = (int)d.C;
-        a.N = (long long)p->total;
-        a.ext = d.ext;
-        a.sq = (unsigned)d.sq;
-        a.ext_bits = d.ext_bits;
-        a.ext_lo = (const cplx<T>*)d.ext_lo;
-        a.ext_hi = (const cplx<T>*)d.ext_hi;
-        for (int k = 0; k < 3; ++k) a.tw[k] = (const cplx<T>*)d.tw[k];
-        a.scale = 1.0;
-        a.has_scale = 0;
-        long long U;
-        if (d.contig) {
-            // signal-major tiles: one run over the batch, W blocks per tile
-            if (per_signal % d.W) return fail(PAFFT_INVALID_ARGUMENT, "fused: blocks per signal %% W");
-            a.ghat = (const cplx<T>*)ghat;
-            a.nsig = 1;
-            a.bps = a.panels;
-            a.tiles_per_panel = 1;
-            a.tiles = a.panels / d.W;
-            U = per_signal / d.W;
-            a.swz = 0;
-            if (d.swz) {
-                const long long tile_bytes = (long long)d.R * d.W * (long long)p->esize;
-                if (tile_bytes % 1024 == 0) {
-                    const long long tr = tile_bytes / 128;
-                    a.swz_b1 = (int)std::min<long long>(tr, 256);
-                    a.swz = (tr % a.swz_b1 == 0 && tr / a.swz_b1 <= 256 &&
-                             ((long long)p->total * (long long)p->esize / 128) % a.swz_b1 == 0)
-                                ? 1
-                                : 0;
-                }
-                if (a.swz) {
-                    d.swz_b1 = a.swz_b1;
-                    ST_TRY(tensor_map_swz(p, d, src, batch, &maps.src[i]));
-                    ST_TRY(tensor_map_swz(p, d, y, batch, &maps.dst[i]));
-                }
-            }
-        } else {
-            a.nsig = (long long)batch;
-            a.bps = per_signal;
-            a.tiles_per_panel = (int)((d.C + d.W - 1) / d.W);
-            a.tiles = a.panels * a.tiles_per_panel;
-            U = per_signal * a.tiles_per_panel;
-            a.use_tmap = 1;
-            a.rb = d.rb;
-            ST_TRY(tensor_map(p, d, src, batch, &maps.src[i]));
-            ST_TRY(tensor_map(p, d, y, batch, &maps.dst[i]));
-        }
-        if (a.tiles > 0x7fffffffll) return fail(PAFFT_INVALID_ARGUMENT, "batch too large for one launch");
-        fa.U[i] = (int)U;
-        total_tiles += a.tiles;
-    }
-    static std::mutex attr_mu;
-    int occ = 0, sms = 0;
-    {
-        std::lock_guard<std::mutex> lk(attr_mu);
-        CUDA_TRY(cudaFuncSetAttribute(fe.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fe.smem));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fe.fn, fe.NT, fe.smem));
-    }
-    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
-    if (occ < 1) return fail(PAFFT_CUDA_ERROR, "fused kernel cannot be resident");
-    const long long grid = std::max<long long>(1, std::min<long long>((long long)occ * sms, total_tiles));
-    // profiling aid: PAFFT_FUSED_ONLY=p runs only pass p's tiles through the
-    // fused machinery (the result is then not a convolution)
-    if (const int only = env_int("PAFFT_FUSED_ONLY", -1); only >= 0 && only < 3)
-        for (int i = 0; i < 3; ++i)
-            if (i != only) fa.U[i] = 0;
-    const int SU = fa.U[0] + fa.U[1] + fa.U[2];
-    // lag: enough tickets between a pass and its consumer that the consumer's
-    // dependency is normally complete when its tickets come up
-    const int lag = std::max(1, env_int("PAFFT_FUSED_LAG", (int)((2 * grid + SU - 1) / SU)));
-    fa.nsig = (int)batch;
-    fa.lag = lag;
-    fa.nticket = ((long long)batch + 2LL * lag) * SU;
-    // per-call counters (stream-ordered): concurrent calls never share them
-    const size_t cbytes = (1 + 3 * batch) * sizeof(unsigned);
-    void* cnt = nullptr;
-    CUDA_TRY(cudaMallocAsync(&cnt, cbytes, st));
-    CUDA_TRY(cudaMemsetAsync(cnt, 0, cbytes, st));
-    fa.ticket = (unsigned*)cnt;
-    fa.done = (unsigned*)cnt + 1;
-    void* args[] = {&fa, &maps};
-    const cudaError_t le = cudaLaunchKernel(fe.fn, dim3((unsigned)grid), dim3(fe.NT), args, fe.smem, st);
-    cudaFreeAsync(cnt, st);
-    CUDA_TRY(le);
-    ++g_launches;
-    return PAFFT_OK;
-}
-
 // ---------------------------------------------------- helper kernels --
 // Out-of-place digit-reversal gather: y[i] = x[(rev_1(i_1), ..., rev_d(i_d))]
 // (permute_tensor, permutation.cpp:46-90, as a pure gather; an involution).
@@ -997,6 +867,8 @@ bool key_match(pafft_filter_t f, pafft_plan_t p) {
         if (f->radices[q] != p->radices[q]) return false;
     for (int q = 0; q < p->rank; ++q)
         if (f->dims[q] != p->dims[q]) return false;
+    for (int i = 0; i < 6; ++i)
+        if (f->layout[i] != p->layout[i]) return false;
     return true;
 }
 
@@ -1154,6 +1026,11 @@ pafft_status pafft_plan_create_mixed(const unsigned* radices, const size_t* dims
     build_groups(p.get());
     // all pass schedules now, so missing kernels surface at plan time
     ST_TRY(passes_permfree(p.get(), p->pf));
+    if (!p->pf.empty()) {
+        const PassDesc& cv = p->pf[p->pf.size() / 2];  // the CONV pass
+        const long long lay[6] = {cv.axis, cv.R, cv.F[0], cv.F[1], cv.F[2], cv.F[3]};
+        for (int i = 0; i < 6; ++i) p->layout[i] = lay[i];
+    }
     ST_TRY(passes_ladder(p.get(), KIND_DIF, p->dif));
     ST_TRY(passes_ladder(p.get(), KIND_DIT_FWD, p->dit_fwd));
     ST_TRY(passes_ladder(p.get(), KIND_DIT_CONJ, p->dit_conj));
@@ -1174,9 +1051,6 @@ pafft_status pafft_plan_create_mixed(const unsigned* radices, const size_t* dims
         p->rev_dev.push_back((uint32_t*)d);
     }
     for (auto& s : p->streams) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    for (auto& s : p->work) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
-    for (auto& e : p->join) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // table uploads above used pageable cudaMemcpy; make them visible to
     // every stream (including non-blocking ones) before the plan is used
     CUDA_TRY(cudaDeviceSynchronize());
@@ -1189,11 +1063,6 @@ pafft_status pafft_plan_destroy(pafft_plan_t plan) {
     cudaSetDevice(plan->device);
     for (auto& s : plan->streams)
         if (s) cudaStreamDestroy(s);
-    for (auto& s : plan->work)
-        if (s) cudaStreamDestroy(s);
-    if (plan->fork) cudaEventDestroy(plan->fork);
-    for (auto& e : plan->join)
-        if (e) cudaEventDestroy(e);
     delete plan;
     return PAFFT_OK;
 }
@@ -1253,6 +1122,7 @@ static pafft_status new_filter(pafft_plan_t p, pafft_filter_t* out) {
     for (int q = 0; q < p->rank; ++q) f->dims[q] = p->dims[q];
     f->prec = p->prec;
     f->device = p->device;
+    for (int i = 0; i < 6; ++i) f->layout[i] = p->layout[i];
     for (std::shared_ptr<DevBuf>* b : {&f->ghat, &f->ghat_scaled}) {
         auto nb = std::make_shared<DevBuf>();
         CUDA_TRY(cudaMalloc(&nb->p, p->total * p->esize ? p->total * p->esize : 16));
@@ -1442,6 +1312,7 @@ pafft_status pafft_filter_broadcast(pafft_filter_t* filters, int ndev, int root,
         const pafft_filter_s& b = *filters[0];
         bool same = a.radix == b.radix && a.rank == b.rank && a.prec == b.prec;
         for (int q = 0; same && q < a.rank; ++q) same = a.dims[q] == b.dims[q] && a.radices[q] == b.radices[q];
+        for (int k = 0; same && k < 6; ++k) same = a.layout[k] == b.layout[k];
         if (!same) return fail(PAFFT_FILTER_PLAN_MISMATCH, "filter %d does not match filter 0's plan key", i);
         for (int j = 0; j < i; ++j)
             if (filters[j]->device == a.device)
@@ -1525,9 +1396,11 @@ struct CacheKey {
     std::vector<unsigned> radices;
     std::vector<size_t> dims;
     int prec, device;
+    std::vector<long long> layout;  // the kernel copy's slot layout (plan's CONV pass)
     unsigned long long h1, h2;
     bool operator<(const CacheKey& o) const {
-        return std::tie(radices, dims, prec, device, h1, h2) < std::tie(o.radices, o.dims, o.prec, o.device, o.h1, o.h2);
+        return std::tie(radices, dims, prec, device, layout, h1, h2) <
+               std::tie(o.radices, o.dims, o.prec, o.device, o.layout, o.h1, o.h2);
     }
 };
 struct CacheEntry {
@@ -1555,7 +1428,7 @@ pafft_status pafft_prepare_filter_from_impulse_cached(pafft_plan_t p, const void
     CUDA_TRY(cudaMemcpyAsync(hh, hb.p, 16, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     CacheKey key{std::vector<unsigned>(p->radices, p->radices + p->rank), std::vector<size_t>(p->dims, p->dims + p->rank),
-                 p->prec, p->device, hh[0], hh[1]};
+                 p->prec, p->device, std::vector<long long>(p->layout, p->layout + 6), hh[0], hh[1]};
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
         auto it = g_cache.find(key);
@@ -1573,6 +1446,7 @@ pafft_status pafft_prepare_filter_from_impulse_cached(pafft_plan_t p, const void
                 }
                 f->prec = p->prec;
                 f->device = p->device;
+                for (int i = 0; i < 6; ++i) f->layout[i] = p->layout[i];
                 f->ghat = std::move(g);
                 f->ghat_scaled = std::move(gs);
                 *out = f.release();
@@ -1645,15 +1519,6 @@ void* pafft_filter_device_ghat_scaled(pafft_filter_t f) { return f ? f->ghat_sca
 int pafft_filter_matches(pafft_filter_t f, pafft_plan_t p) { return f && p && key_match(f, p) ? 1 : 0; }
 
 // ------------------------------------------------------------- hot path
-// Signals per L2-resident chunk: all passes of a chunk run back to back so the
-// intermediate passes hit L2 (126 MB) instead of HBM; two chunks are in
-// flight on two internal streams, next to the resident filter.
-static size_t chunk_signals(pafft_plan_t p) {
-    const size_t sig = p->total * p->esize;
-    const size_t budget = (size_t)env_int("PAFFT_CHUNK_MB", 36) << 20;
-    return std::max<size_t>(1, budget / std::max<size_t>(sig, 1));
-}
-
 pafft_status pafft_convolve_permfree_oop(pafft_plan_t p, pafft_filter_t f, const void* x_dev, void* y_dev,
                                          size_t batch, void* stream) {
     if (!p || !f) return fail(PAFFT_INVALID_ARGUMENT, "null plan or filter");
@@ -1666,41 +1531,9 @@ pafft_status pafft_convolve_permfree_oop(pafft_plan_t p, pafft_filter_t f, const
     cudaStream_t st = (cudaStream_t)stream;
     const std::vector<PassDesc>& ps = p->pf;
     if (ps.empty()) return hadamard_dev(p, x_dev, f->ghat_scaled->p, y_dev, batch, st);
-    const size_t chunk = chunk_signals(p);
-    // measured on B200 (config 2): one-chunk launches lose more to tails than
-    // L2 residency saves, so the chunk pipeline is opt-in (PAFFT_PIPELINE=1)
-    const bool pipeline = ps.size() > 1 && batch > chunk && env_int("PAFFT_PIPELINE", 0) != 0;
-    if (env_int("PAFFT_FUSED", 0) != 0) {
-        if (const FusedEntry* fe = fused_entry(p)) return launch_fused(p, *fe, f->ghat_scaled->p, x_dev, y_dev, batch, st);
-    }
-    if (!pipeline) {
-        for (size_t i = 0; i < ps.size(); ++i)
-            ST_TRY(launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch,
-                          ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr, nullptr, 1.0, st));
-        return PAFFT_OK;
-    }
-    // fork: both work streams wait for everything already queued on `st`
-    CUDA_TRY(cudaEventRecord(p->fork, st));
-    for (auto& w : p->work) CUDA_TRY(cudaStreamWaitEvent(w, p->fork, 0));
-    const size_t sig = p->total * p->esize;
-    int k = 0;
-    for (size_t done = 0; done < batch; done += chunk, ++k) {
-        const size_t nb = std::min(chunk, batch - done);
-        cudaStream_t w = p->work[k & 1];
-        const char* xs = (const char*)x_dev + done * sig;
-        char* ys = (char*)y_dev + done * sig;
-        for (size_t i = 0; i < ps.size(); ++i) {
-            // half the resident CTA slots each, so the two chunks run side by side
-            const long long cap = std::max<long long>(1, ps[i].max_ctas / 2);
-            ST_TRY(launch(p, ps[i], i == 0 ? (const void*)xs : (const void*)ys, ys, nb,
-                          ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr, nullptr, 1.0, w, cap));
-        }
-    }
-    // join
-    for (int i = 0; i < 2; ++i) {
-        CUDA_TRY(cudaEventRecord(p->join[i], p->work[i]));
-        CUDA_TRY(cudaStreamWaitEvent(st, p->join[i], 0));
-    }
+    for (size_t i = 0; i < ps.size(); ++i)
+        ST_TRY(launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch,
+                      ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr, nullptr, 1.0, st));
     return PAFFT_OK;
 }
 
@@ -1719,11 +1552,6 @@ pafft_status pafft_convolve_permfree_pass(pafft_plan_t p, pafft_filter_t f, cons
     // passes on disjoint SM sets, tools/corun_probe.py)
     return launch(p, ps[i], i == 0 ? x_dev : y_dev, y_dev, batch, ps[i].kind == KIND_CONV ? f->ghat_scaled->p : nullptr,
                   nullptr, 1.0, (cudaStream_t)stream, env_int("PAFFT_PASS_GRID_CAP", 0));
-}
-
-size_t pafft_plan_chunk_signals(pafft_plan_t p) {
-    if (!p) return 0;
-    return env_int("PAFFT_PIPELINE", 0) != 0 ? chunk_signals(p) : 0;  // 0: whole batch per launch
 }
 
 pafft_status pafft_plan_pass_info(pafft_plan_t p, int i, int* kind, int* axis, int* R, int* stages) {

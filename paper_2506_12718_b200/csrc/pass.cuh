@@ -331,33 +331,6 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// L2 prefetch of a tile that will be staged one tile later (TMA prefetch,
-// no shared memory): its DRAM reads start a whole tile earlier, so the later
-// bulk/tensor load is served from L2.  Called by one thread.  Off by default:
-// measured on B200 it slows the strided passes (config 4 -5..8%) and gains
-// <= 4% on contiguous ones.
-#ifndef PAFFT_L2PF
-#define PAFFT_L2PF 0
-#endif
-template <int R, int W, bool STRIDED, typename T>
-__device__ __forceinline__ void prefetch_tile_l2(const PassArgs<T>& a, const CUtensorMap* map, long long tile) {
-    using V = cplx<T>;
-    const TileGeo g = tile_geo<R, W, STRIDED>(a, tile);
-    if (STRIDED && a.use_tmap) {
-        const unsigned p = (unsigned)tile / (unsigned)a.tiles_per_panel;
-        asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(map),
-                     "r"((int)(2 * g.first)), "r"(0), "r"((int)(p * (R / a.rb)))
-                     : "memory");
-    } else if (!STRIDED && a.swz) {
-        asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(map), "r"(0), "r"(0),
-                     "r"((int)(g.base * (long long)sizeof(V) / 128 / a.swz_b1))
-                     : "memory");
-    } else if (!STRIDED) {
-        const unsigned bytes = (unsigned)((long long)g.nvalid * R * sizeof(V)) & ~15u;
-        if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.src + g.base), "r"(bytes) : "memory");
-    }
-}
-
 template <int R, int W, int SW, typename T>
 __device__ __noinline__ void stage_rows(const PassArgs<T>& a, const TileGeo g, cplx<T>* buf, unsigned long long* bar,
                                         int lane) {
@@ -567,7 +540,7 @@ template <typename FA, int RADIX, int GPW> __constant__ ScatterMap<FA, RADIX, GP
 // the column transforms, the epilogue, and the issue of the tile's bulk/tensor
 // store (committed as one bulk group by warp 0 lane 0).  `service` is called by
 // every thread after the tile's first internal barrier (the deferred refill).
-// Threads t >= Pol::NT (a fused kernel's wider CTA) only join the barriers.
+// Threads t >= Pol::NT (a CTA wider than the tile needs) only join the barriers.
 template <typename T, int RADIX, typename FA, int KIND, int MAP, typename Pol, bool ALL_ACTIVE, typename Svc>
 __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap* tmap_dst, long long tile,
                                          cplx<T>* buf, const cplx<T>* buf_end, int t, Svc&& service,
@@ -889,7 +862,6 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
         if (t0 < a.tiles) stage_tile<R, W, SW, STRIDED>(a, &tmap, t0, bufs, &bars[0], lane);
         if (NBUF == 2 && t0 + ts < a.tiles)
             stage_tile<R, W, SW, STRIDED>(a, &tmap, t0 + ts, bufs + BUFE, &bars[1], lane);
-        if (PAFFT_L2PF && lane == 0 && t0 + NBUF * ts < a.tiles) prefetch_tile_l2<R, W, STRIDED>(a, &tmap, t0 + NBUF * ts);
     }
     __syncthreads();  // hand-copied fp32 tail elements of the first tiles
 
@@ -905,7 +877,6 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
             __syncwarp();
             fence_proxy_async();
             stage_tile<R, W, SW, STRIDED>(a, &tmap, pend, pbuf, pbar, lane);
-            if (PAFFT_L2PF && lane == 0 && pend + ts < a.tiles) prefetch_tile_l2<R, W, STRIDED>(a, &tmap, pend + ts);
             if constexpr (KIND == KIND_CONV && PAFFT_GHAT_PF && FA::FMAX < 25) {
                 // the staged tile's filter blocks into L2 ahead of the multiply:
                 // measured on B200 config 4 (256 MiB filter) CONV -9%, config 2

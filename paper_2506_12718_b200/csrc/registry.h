@@ -19,19 +19,6 @@ struct KernelEntry {
 
 using Registry = std::vector<KernelEntry>;
 
-// Fused convolution kernels (fused.cuh): strided split R_D (tile width WD) and
-// contiguous split R_C (WC blocks per tile) in one persistent launch.
-struct FusedEntry {
-    int prec;
-    int radix;
-    int RD, RC;
-    int WD, WC;
-    int NT, smem;
-    const void* fn;
-};
-using FusedRegistry = std::vector<FusedEntry>;
-void register_fused_f64(FusedRegistry&);
-
 void register_r2_f64(Registry&);
 void register_r3_f64(Registry&);
 void register_r4_f64(Registry&);

@@ -77,11 +77,15 @@ def _pf():
     return pf
 
 
-def impulse(cfg: Config) -> np.ndarray:
-    """The filter's impulse response h (vec order, complex128)."""
+def impulse(cfg: Config, fill_normal=None) -> np.ndarray:
+    """The filter's impulse response h (vec order, complex128).  `fill_normal`
+    (seed, n) -> complex128 defaults to the product library's SplitMix64
+    generator; the reference arm of bench.py passes the oracle's, which emits
+    the same bytes (tests/test_abi.py), so that process never maps this package's
+    library."""
     n = cfg.total
     if cfg.filt == "cnormal":
-        return _pf().fill_normal(seed_filter(), n)
+        return (fill_normal or _pf().fill_normal)(seed_filter(), n)
     if cfg.filt == "gauss2d":
         n1, n2 = cfg.dims
         d1 = np.minimum(np.arange(n1), n1 - np.arange(n1)).astype(np.float64)
@@ -141,8 +145,18 @@ def signal_bytes(cfg: Config) -> int:
     return cfg.total * (16 if cfg.precision == "f64" else 8)
 
 
-def bytes_per_conv(cfg: Config, gpus: int = 1) -> float:
+def shard_count(cfg: Config, gpus: int = 1, weak: bool = False) -> int:
+    """B_g: convolutions per GPU sharing one resident ghat.
+    Batched configs split the fixed global batch (batch / G, the largest shard
+    when G does not divide it); config 1's call sequence runs as replicas."""
+    if cfg.calls > 1:
+        return cfg.calls
+    if weak:
+        return max(1, cfg.batch)
+    return max(1, -(-cfg.batch // max(1, gpus)))
+
+
+def bytes_per_conv(cfg: Config, gpus: int = 1, weak: bool = False) -> float:
     """B_alg = 2 S + S / B_g: read x once, write y once, ghat once per GPU per step."""
     S = signal_bytes(cfg)
-    bg = cfg.calls if cfg.calls > 1 else max(1, cfg.batch)
-    return 2.0 * S + S / bg
+    return 2.0 * S + S / shard_count(cfg, gpus, weak)

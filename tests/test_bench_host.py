@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _reference_arm(config):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config",
-                        str(config), "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                        str(config), "--steps", "1", "--warmup", "0", "--no-sub"], capture_output=True, text=True,
                        timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -39,6 +39,11 @@ def test_reference_arm_contract(config, kind):
     cb = d["cpu_baseline"]
     assert cb["kind"] == kind and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # the reference arm times the full config batch and never maps the product library
+    from paper_2506_12718_b200 import workload
+    cfg = workload.get_config(config)
+    assert d["config"]["global_batch"] == (cfg.calls if cfg.calls > 1 else cfg.batch)
+    assert d["repo_libs_loaded"] and all(p.startswith("oracle/") for p in d["repo_libs_loaded"])
 
 
 def test_bench_ops_parse_dims():
