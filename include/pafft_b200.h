@@ -83,6 +83,13 @@ pafft_status pafft_digit_reverse(uint64_t j, unsigned radix, unsigned digits, ui
  * The observable ghat (PreparedFilter::ghat) is kept bit-exact. */
 pafft_status pafft_prepare_filter_split(pafft_plan_t plan, const double* g_re, const double* g_im,
                                         pafft_filter_t* out);
+/* A filter whose spectrum is ALREADY digit-reversed (a PreparedFilter::ghat
+ * the caller built or edited, convolution.hpp:9-12): uploaded as is, no
+ * reordering pass.  The C++ shim uses it for aggregate-initialised or edited
+ * PreparedFilter objects, since the reference reads ghat directly
+ * (convolution.cpp:45-52). */
+pafft_status pafft_filter_from_prepared_split(pafft_plan_t plan, const double* ghat_re, const double* ghat_im,
+                                              pafft_filter_t* out);
 /* Same from a device-resident interleaved spectrum (same precision as plan). */
 pafft_status pafft_prepare_filter_device(pafft_plan_t plan, const void* g_dev, void* stream,
                                          pafft_filter_t* out);
@@ -153,6 +160,14 @@ pafft_status pafft_plan_pass_info(pafft_plan_t plan, int i, int* kind, int* axis
  * D2H inside.  Mirrors convolve_permfree(ComplexBuffer&, ...) exactly. */
 pafft_status pafft_convolve_permfree_split(pafft_plan_t plan, pafft_filter_t filter, double* re, double* im,
                                            size_t batch);
+/* As pafft_convolve_permfree_split, but once the device result is ready the
+ * library calls commit(ctx) and writes re/im back only if it returns nonzero
+ * (*committed says which; re/im are untouched otherwise).  The C++ drop-in
+ * uses it to check, concurrently with the upload and the convolution, that
+ * the device spectrum still equals PreparedFilter::ghat (the reference reads
+ * ghat on every call, convolution.cpp:49) without a serial pass over it. */
+pafft_status pafft_convolve_permfree_split_if(pafft_plan_t plan, pafft_filter_t filter, double* re, double* im,
+                                              size_t batch, int (*commit)(void*), void* ctx, int* committed);
 /* Host interleaved buffers (pinned or pageable), pipelined in chunks over
  * copy/compute streams; synchronous. In place on x_host. */
 pafft_status pafft_convolve_permfree_host(pafft_plan_t plan, pafft_filter_t filter, void* x_host,

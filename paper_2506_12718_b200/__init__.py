@@ -132,7 +132,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # (module globals may be gone at interpreter exit)
             lib.pafft_plan_destroy(h)
             self._h = None
 
@@ -190,7 +190,7 @@ class PreparedFilter:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:
             lib.pafft_filter_destroy(h)
             self._h = None
 

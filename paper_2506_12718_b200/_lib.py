@@ -39,6 +39,8 @@ _SIGS = {
     "pafft_plan_describe": ([_vp, C.c_char_p, _sz], _st),
     "pafft_digit_reverse": ([C.c_uint64, C.c_uint, C.c_uint, C.POINTER(C.c_uint64)], _st),
     "pafft_prepare_filter_split": ([_vp, _dp, _dp, C.POINTER(_vp)], _st),
+    "pafft_filter_from_prepared_split": ([_vp, _dp, _dp, C.POINTER(_vp)], _st),
+    "pafft_convolve_permfree_split_if": ([_vp, _vp, _dp, _dp, _sz, _vp, _vp, C.POINTER(C.c_int)], _st),
     "pafft_prepare_filter_device": ([_vp, _vp, _vp, C.POINTER(_vp)], _st),
     "pafft_prepare_filter_from_impulse_device": ([_vp, _vp, _vp, C.POINTER(_vp)], _st),
     "pafft_prepare_filter_from_impulse_cached": ([_vp, _vp, _vp, C.POINTER(_vp), C.POINTER(C.c_int)], _st),

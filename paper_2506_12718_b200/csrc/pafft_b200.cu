@@ -78,20 +78,23 @@ Registry& registry() {
         register_r4_f32(reg);
         register_r5_f32(reg);
         register_r8_f32(reg);
+        register_narrow_f64(reg);
+        register_narrow_f32(reg);
     });
     return reg;
 }
 
-const KernelEntry* find_kernel(int prec, int radix, int R, int kind, int map) {
+const KernelEntry* find_kernel(int prec, int radix, int R, int kind, int map, int wovr = 0) {
     for (const auto& e : registry())
-        if (e.prec == prec && e.radix == radix && e.R == R && e.kind == kind && e.map == map) return &e;
+        if (e.prec == prec && e.radix == radix && e.R == R && e.kind == kind && e.map == map && e.wovr == wovr)
+            return &e;
     return nullptr;
 }
 
 int max_stages_compiled(int prec, int radix, int kind, int map) {
     int best = 0;
     for (const auto& e : registry()) {
-        if (e.radix != radix || e.prec != prec || e.kind != kind || e.map != map) continue;
+        if (e.radix != radix || e.prec != prec || e.kind != kind || e.map != map || e.wovr) continue;
         int s = 0;
         for (int v = e.R; v > 1; v /= radix) ++s;
         best = std::max(best, s);
@@ -131,14 +134,6 @@ struct AsyncBuf {
     }
 };
 
-// Per-call stream for the synchronous host-buffer entry points.
-struct CallStream {
-    cudaStream_t s = nullptr;
-    ~CallStream() {
-        if (s) cudaStreamDestroy(s);
-    }
-};
-
 struct PassDesc {
     int kind = 0;
     int axis = 0, a = 0, s = 0;
@@ -155,6 +150,9 @@ struct PassDesc {
     const void* ext_hi = nullptr;
     const void* tw[3] = {nullptr, nullptr, nullptr};
     const void* fn = nullptr;
+    // narrow-tile variant of a strided pass (fewer columns per tile), taken by
+    // launches whose default tiles would not fill the SMs (use_narrow)
+    std::shared_ptr<PassDesc> narrow;
 };
 
 struct Group {
@@ -353,6 +351,29 @@ void build_groups(pafft_plan_t p) {
     // contiguous one ends the list even if axis 0 has extent 1.
 }
 
+// The kernel-instance part of a pass: entry point, codelet split, tile
+// policy, and the persistent grid (every resident CTA slot, no more).
+pafft_status bind_kernel(pafft_plan_t p, const KernelEntry& ke, PassDesc& d) {
+    d.fn = ke.fn;
+    d.F[0] = ke.F0;
+    d.F[1] = ke.F1;
+    d.F[2] = ke.F2;
+    d.F[3] = ke.F3;
+    d.nsteps = 1 + (d.F[1] > 1) + (d.F[2] > 1) + (d.F[3] > 1);
+    d.W = ke.W;
+    d.NT = ke.NT;
+    d.smem = (size_t)ke.smem;
+    if (d.smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(d.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
+    int occ = 0, sms = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, d.fn, d.NT, d.smem));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+    if (occ < 1) return fail(PAFFT_CUDA_ERROR, "pass kernel R=%d cannot be resident (smem %zu)", d.R, d.smem);
+    d.max_ctas = (long long)occ * sms;
+    if (!d.contig) d.sw = p->esize == 8 ? d.W + 2 : d.W;
+    return PAFFT_OK;
+}
+
 pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     const long long n = (long long)p->dims[g.axis];
     long long sq = 1;
@@ -372,25 +393,7 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     if (!ke)
         return fail(PAFFT_INVALID_ARGUMENT, "no kernel for radix %u R=%d kind %d map %d", radix, d.R, kind,
                     d.contig);
-    d.fn = ke->fn;
-    d.F[0] = ke->F0;
-    d.F[1] = ke->F1;
-    d.F[2] = ke->F2;
-    d.F[3] = ke->F3;
-    d.nsteps = 1 + (d.F[1] > 1) + (d.F[2] > 1) + (d.F[3] > 1);
-    d.W = ke->W;
-    d.NT = ke->NT;
-    d.smem = (size_t)ke->smem;
-    if (d.smem > 48 * 1024)
-        CUDA_TRY(cudaFuncSetAttribute(d.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
-    {
-        // persistent grid: every resident CTA slot on the device, no more
-        int occ = 0, sms = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, d.fn, d.NT, d.smem));
-        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
-        if (occ < 1) return fail(PAFFT_CUDA_ERROR, "pass kernel R=%d cannot be resident (smem %zu)", d.R, d.smem);
-        d.max_ctas = (long long)occ * sms;
-    }
+    ST_TRY(bind_kernel(p, *ke, d));
     if (d.contig && (radix == 2 || radix == 4 || radix == 8) && env_int("PAFFT_NO_SWIZZLE", 0) == 0) {
         const long long tile_bytes = (long long)d.R * d.W * (long long)p->esize;
         if (tile_bytes % 1024 == 0) {
@@ -401,8 +404,7 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     }
     if (!d.contig) {
         // 2-D tensor map staging needs 16-byte row strides (always for fp64,
-        // even C for fp32); otherwise one bulk copy per row.
-        d.sw = p->esize == 8 ? d.W + 2 : d.W;
+        // even C for fp32); otherwise one bulk copy per row (d.sw: bind_kernel).
         // fp64 strided tiles always stage and store through tensor maps (their
         // tile store is a tensor store); fp32 ones may use per-row copies
         d.use_tmap = p->esize == 16 || ((d.C % 2) == 0 && env_int("PAFFT_NO_TMAP", 0) == 0);
@@ -418,6 +420,19 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     d.ext = d.L > 1;
     if (d.ext) ST_TRY(ext_table(p, d.K0, d));
     if (d.nsteps > 1) ST_TRY(int_table(p, d));
+    if (!d.contig) {
+        // narrow-tile variant (W = PAFFT_NARROW_W, default 4 fp64 / 8 fp32
+        // columns), when compiled for this stage group and narrower than the
+        // default tile
+        const int nw = env_int("PAFFT_NARROW_W", p->esize == 16 ? 4 : 8);
+        const KernelEntry* ne = nw > 0 ? find_kernel(p->prec, (int)radix, d.R, kind, MAP_STRIDED, nw) : nullptr;
+        if (ne && ne->W < d.W && ne->F0 == d.F[0] && ne->F1 == d.F[1] && ne->F2 == d.F[2] && ne->F3 == d.F[3]) {
+            auto nd = std::make_shared<PassDesc>(d);
+            nd->narrow.reset();
+            ST_TRY(bind_kernel(p, *ne, *nd));
+            d.narrow = nd;
+        }
+    }
     return PAFFT_OK;
 }
 
@@ -564,8 +579,22 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     return PAFFT_OK;
 }
 
-pafft_status launch(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
+// A strided launch takes its narrow-tile variant when the default tiles are
+// fewer than two per resident CTA slot: one ragged wave in which most SMs hold
+// one or two large tiles and no tile pipelining happens (a batch-1 2^20
+// signal: 512 default tiles for 444 slots).  PAFFT_NARROW=0/1 forces it off/on.
+bool use_narrow(const PassDesc& d, const pafft_plan_s* p, size_t batch) {
+    if (!d.narrow) return false;
+    const int force = env_int("PAFFT_NARROW", -1);
+    if (force >= 0) return force != 0;
+    const long long per_signal = (long long)p->total / ((long long)d.R * d.C);
+    const long long tiles = per_signal * (long long)batch * ((d.C + d.W - 1) / d.W);
+    return tiles < 2 * d.max_ctas;
+}
+
+pafft_status launch(pafft_plan_t p, const PassDesc& d0, const void* src, void* dst, size_t batch,
                     const void* ghat, const void* mul, double scale, cudaStream_t st, long long grid_cap = 0) {
+    const PassDesc& d = use_narrow(d0, p, batch) ? *d0.narrow : d0;
     return p->prec == 0 ? launch_t<double>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap)
                         : launch_t<float>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap);
 }
@@ -930,6 +959,80 @@ pafft_status run_ladder(pafft_plan_t p, const std::vector<PassDesc>& ps, const v
 }  // namespace
 
 // ===================================================================== ABI
+// ------------------------------------------------ split (drop-in) I/O
+// The reference API holds a signal as split host arrays (ComplexBuffer re/im,
+// core.hpp:48-63).  The synchronous split entry points copy re and im as two
+// plain host->device copies into stream-ordered pool scratch and (de)interleave
+// on the device (converting to fp32 for fp32 plans), on a thread-local stream
+// per device: no cudaMalloc, no stream creation and no host interleave loop per
+// call, and calls from distinct threads run concurrently.
+template <typename T>
+__global__ void split_to_cplx_kernel(const double* __restrict__ re, const double* __restrict__ im,
+                                     cplx<T>* __restrict__ out, unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        out[i] = cplx<T>{(T)re[i], (T)im[i]};
+}
+template <typename T>
+__global__ void cplx_to_split_kernel(const cplx<T>* __restrict__ in, double* __restrict__ re,
+                                     double* __restrict__ im, unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const cplx<T> v = in[i];
+        re[i] = (double)v.x;
+        im[i] = (double)v.y;
+    }
+}
+
+static pafft_status call_stream(int device, cudaStream_t* out) {
+    thread_local std::vector<cudaStream_t> streams;  // never destroyed: live for the thread
+    if ((int)streams.size() <= device) streams.resize(device + 1, nullptr);
+    if (!streams[device]) CUDA_TRY(cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking));
+    *out = streams[device];
+    return PAFFT_OK;
+}
+
+template <typename T>
+static pafft_status upload_split_as(pafft_plan_t p, const double* re, const double* im, size_t n, cplx<T>* dev,
+                                    cudaStream_t st) {
+    AsyncBuf sc;
+    ST_TRY(async_alloc(p, sc, 2 * n * sizeof(double), st));
+    double* dre = (double*)sc.p;
+    double* dim = dre + n;
+    CUDA_TRY(cudaMemcpyAsync(dre, re, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dim, im, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    split_to_cplx_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(dre, dim, dev, n);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    return PAFFT_OK;
+}
+template <typename T>
+static pafft_status download_split_as(pafft_plan_t p, const cplx<T>* dev, size_t n, double* re, double* im,
+                                      cudaStream_t st) {
+    AsyncBuf sc;
+    ST_TRY(async_alloc(p, sc, 2 * n * sizeof(double), st));
+    double* dre = (double*)sc.p;
+    double* dim = dre + n;
+    cplx_to_split_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(dev, dre, dim, n);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    CUDA_TRY(cudaMemcpyAsync(re, dre, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(im, dim, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return PAFFT_OK;
+}
+// plan precision
+static pafft_status upload_split(pafft_plan_t p, const double* re, const double* im, size_t n, void* dev,
+                                 cudaStream_t st) {
+    return p->prec == 0 ? upload_split_as<double>(p, re, im, n, (double2*)dev, st)
+                        : upload_split_as<float>(p, re, im, n, (float2*)dev, st);
+}
+static pafft_status download_split(pafft_plan_t p, const void* dev, size_t n, double* re, double* im,
+                                   cudaStream_t st) {
+    return p->prec == 0 ? download_split_as<double>(p, (const double2*)dev, n, re, im, st)
+                        : download_split_as<float>(p, (const float2*)dev, n, re, im, st);
+}
+
 extern "C" {
 
 const char* pafft_last_error(void) { return g_err.c_str(); }
@@ -1104,6 +1207,11 @@ pafft_status pafft_plan_describe(pafft_plan_t p, char* buf, size_t len) {
                  kn[d.kind], d.axis, d.a, d.a + d.s, d.R, d.F[0], d.F[1], d.F[2], d.F[3], d.K0, d.L, d.C,
                  d.contig ? "contig" : "strided", d.W, d.NT, d.smem, d.ext);
         s += line;
+        if (d.narrow) {
+            snprintf(line, sizeof line, "  (few tiles: W=%d NT=%d smem=%zu slots=%lld)\n", d.narrow->W, d.narrow->NT,
+                     d.narrow->smem, d.narrow->max_ctas);
+            s += line;
+        }
     }
     if (buf && len) {
         strncpy(buf, s.c_str(), len - 1);
@@ -1192,17 +1300,14 @@ pafft_status pafft_prepare_filter_split(pafft_plan_t p, const double* g_re, cons
                                         pafft_filter_t* out) {
     if (!p || !out || !g_re || !g_im) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
     ST_TRY(set_device(p));
+    cudaStream_t st;
+    ST_TRY(call_stream(p->device, &st));
     const size_t n = p->total;
-    std::vector<double> h(2 * n);
-    for (size_t i = 0; i < n; ++i) {
-        h[2 * i] = g_re[i];
-        h[2 * i + 1] = g_im[i];
-    }
     // the observable ghat stays bit-exact: permute in double, convert after
-    DevBuf g64, gh64;
-    CUDA_TRY(cudaMalloc(&g64.p, n * 16));
-    CUDA_TRY(cudaMalloc(&gh64.p, n * 16));
-    CUDA_TRY(cudaMemcpy(g64.p, h.data(), n * 16, cudaMemcpyHostToDevice));
+    AsyncBuf g64, gh64;
+    ST_TRY(async_alloc(p, g64, n * 16, st));
+    ST_TRY(async_alloc(p, gh64, n * 16, st));
+    ST_TRY(upload_split_as<double>(p, g_re, g_im, n, (double2*)g64.p, st));
     pafft_filter_t f;
     ST_TRY(new_filter(p, &f));
     std::unique_ptr<pafft_filter_s> guard(f);
@@ -1214,22 +1319,38 @@ pafft_status pafft_prepare_filter_split(pafft_plan_t p, const double* g_re, cons
             pa.dims[q] = p->dims[q];
             pa.rev[q] = p->rev_dev[q];
         }
-        permute_kernel<double2><<<grid_for(n, 256), 256>>>((const double2*)g64.p, (double2*)gh64.p, n, n, pa);
+        permute_kernel<double2><<<grid_for(n, 256), 256, 0, st>>>((const double2*)g64.p, (double2*)gh64.p, n, n, pa);
         CUDA_TRY(cudaGetLastError());
         ++g_launches;
-        ++g_perm_passes;
+        ++g_perm_passes;  // the one offline reordering pass (convolution.cpp:9-14)
     }
     if (p->prec == 0)
-        CUDA_TRY(cudaMemcpy(f->ghat->p, gh64.p, n * 16, cudaMemcpyDeviceToDevice));
+        CUDA_TRY(cudaMemcpyAsync(f->ghat->p, gh64.p, n * 16, cudaMemcpyDeviceToDevice, st));
     else {
-        scale_convert_kernel<float><<<grid_for(n, 256), 256>>>((const double2*)gh64.p, (float2*)f->ghat->p,
-                                                               (float2*)f->ghat_scaled->p, 1.0, n);
+        scale_convert_kernel<float><<<grid_for(n, 256), 256, 0, st>>>((const double2*)gh64.p, (float2*)f->ghat->p,
+                                                                      (float2*)f->ghat_scaled->p, 1.0, n);
         CUDA_TRY(cudaGetLastError());
         ++g_launches;
     }
-    CUDA_TRY(cudaDeviceSynchronize());
-    ST_TRY(pafft_filter_sync_scaled(f, nullptr));
-    CUDA_TRY(cudaDeviceSynchronize());
+    ST_TRY(pafft_filter_sync_scaled(f, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    *out = guard.release();
+    return PAFFT_OK;
+}
+
+pafft_status pafft_filter_from_prepared_split(pafft_plan_t p, const double* ghat_re, const double* ghat_im,
+                                              pafft_filter_t* out) {
+    if (!p || !out || !ghat_re || !ghat_im) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
+    ST_TRY(set_device(p));
+    cudaStream_t st;
+    ST_TRY(call_stream(p->device, &st));
+    pafft_filter_t f;
+    ST_TRY(new_filter(p, &f));
+    std::unique_ptr<pafft_filter_s> guard(f);
+    // already digit-reversed: no reordering pass
+    ST_TRY(upload_split(p, ghat_re, ghat_im, p->total, f->ghat->p, st));
+    ST_TRY(pafft_filter_sync_scaled(f, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     *out = guard.release();
     return PAFFT_OK;
 }
@@ -1491,26 +1612,12 @@ pafft_status pafft_filter_destroy(pafft_filter_t f) {
 }
 
 pafft_status pafft_filter_ghat_split(pafft_filter_t f, double* re, double* im) {
-    if (!f) return fail(PAFFT_INVALID_ARGUMENT, "null filter");
+    if (!f || !re || !im) return fail(PAFFT_INVALID_ARGUMENT, "null argument");
     pafft_plan_t p = f->plan;
     ST_TRY(set_device(p));
-    const size_t n = p->total;
-    if (p->prec == 0) {
-        std::vector<double> h(2 * n);
-        CUDA_TRY(cudaMemcpy(h.data(), f->ghat->p, n * 16, cudaMemcpyDeviceToHost));
-        for (size_t i = 0; i < n; ++i) {
-            re[i] = h[2 * i];
-            im[i] = h[2 * i + 1];
-        }
-    } else {
-        std::vector<float> h(2 * n);
-        CUDA_TRY(cudaMemcpy(h.data(), f->ghat->p, n * 8, cudaMemcpyDeviceToHost));
-        for (size_t i = 0; i < n; ++i) {
-            re[i] = h[2 * i];
-            im[i] = h[2 * i + 1];
-        }
-    }
-    return PAFFT_OK;
+    cudaStream_t st;
+    ST_TRY(call_stream(p->device, &st));
+    return download_split(p, f->ghat->p, p->total, re, im, st);
 }
 
 void* pafft_filter_device_ghat(pafft_filter_t f) { return f ? f->ghat->p : nullptr; }
@@ -1569,68 +1676,39 @@ pafft_status pafft_convolve_permfree(pafft_plan_t p, pafft_filter_t f, void* x_d
     return pafft_convolve_permfree_oop(p, f, x_dev, x_dev, batch, stream);
 }
 
-static void interleave(const double* re, const double* im, size_t n, double* out) {
-    for (size_t i = 0; i < n; ++i) {
-        out[2 * i] = re[i];
-        out[2 * i + 1] = im[i];
+pafft_status pafft_convolve_permfree_split_if(pafft_plan_t p, pafft_filter_t f, double* re, double* im,
+                                              size_t batch, int (*commit)(void*), void* ctx, int* committed) {
+    if (committed) *committed = 0;
+    if (!p || !f) return fail(PAFFT_INVALID_ARGUMENT, "null plan or filter");
+    if (!key_match(f, p)) return fail(PAFFT_FILTER_PLAN_MISMATCH, "prepared filter does not belong to this plan");
+    if (batch == 0) {
+        if (committed) *committed = 1;
+        return PAFFT_OK;
     }
-}
-static void deinterleave(const double* in, size_t n, double* re, double* im) {
-    for (size_t i = 0; i < n; ++i) {
-        re[i] = in[2 * i];
-        im[i] = in[2 * i + 1];
-    }
-}
-
-// host split <-> device (plan precision) helpers
-// All host<->device traffic of the split (drop-in) paths is ordered on the
-// plan's own stream; the non-blocking plan streams do not synchronise with the
-// legacy default stream, so a plain cudaMemcpy would race the kernels.
-static pafft_status upload_split(pafft_plan_t p, const double* re, const double* im, size_t n, void* dev,
-                                 cudaStream_t st) {
-    std::vector<double> h(2 * n);
-    interleave(re, im, n, h.data());
-    if (p->prec == 0) {
-        CUDA_TRY(cudaMemcpyAsync(dev, h.data(), n * 16, cudaMemcpyHostToDevice, st));
-    } else {
-        std::vector<float> f(2 * n);
-        for (size_t i = 0; i < 2 * n; ++i) f[i] = (float)h[i];
-        CUDA_TRY(cudaMemcpyAsync(dev, f.data(), n * 8, cudaMemcpyHostToDevice, st));
-    }
-    CUDA_TRY(cudaStreamSynchronize(st));
-    return PAFFT_OK;
-}
-static pafft_status download_split(pafft_plan_t p, const void* dev, size_t n, double* re, double* im,
-                                   cudaStream_t st) {
-    std::vector<double> h(2 * n);
-    if (p->prec == 0) {
-        CUDA_TRY(cudaMemcpyAsync(h.data(), dev, n * 16, cudaMemcpyDeviceToHost, st));
-    } else {
-        std::vector<float> f(2 * n);
-        CUDA_TRY(cudaMemcpyAsync(f.data(), dev, n * 8, cudaMemcpyDeviceToHost, st));
+    if (!re || !im) return fail(PAFFT_INVALID_ARGUMENT, "null buffer");
+    ST_TRY(set_device(p));
+    cudaStream_t st;
+    ST_TRY(call_stream(p->device, &st));
+    const size_t n = p->total * batch;
+    AsyncBuf x;
+    ST_TRY(async_alloc(p, x, n * p->esize, st));
+    ST_TRY(upload_split(p, re, im, n, x.p, st));
+    ST_TRY(pafft_convolve_permfree(p, f, x.p, batch, st));
+    // the caller's veto (the C++ shim's check that the filter's spectrum still
+    // equals PreparedFilter::ghat, run on another thread while the upload and
+    // the convolution were in flight): the host arrays are written only on commit
+    if (commit && !commit(ctx)) {
         CUDA_TRY(cudaStreamSynchronize(st));
-        for (size_t i = 0; i < 2 * n; ++i) h[i] = f[i];
+        return PAFFT_OK;
     }
-    CUDA_TRY(cudaStreamSynchronize(st));
-    deinterleave(h.data(), n, re, im);
+    ST_TRY(download_split(p, x.p, n, re, im, st));
+    if (committed) *committed = 1;
     return PAFFT_OK;
 }
 
 pafft_status pafft_convolve_permfree_split(pafft_plan_t p, pafft_filter_t f, double* re, double* im,
                                            size_t batch) {
-    if (!p || !f) return fail(PAFFT_INVALID_ARGUMENT, "null plan or filter");
-    if (!key_match(f, p)) return fail(PAFFT_FILTER_PLAN_MISMATCH, "prepared filter does not belong to this plan");
-    if (batch == 0) return PAFFT_OK;
-    ST_TRY(set_device(p));
-    const size_t n = p->total * batch;
-    DevBuf x;
-    CUDA_TRY(cudaMalloc(&x.p, n * p->esize));
-    CallStream cs;
-    CUDA_TRY(cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking));
-    ST_TRY(upload_split(p, re, im, n, x.p, cs.s));
-    ST_TRY(pafft_convolve_permfree(p, f, x.p, batch, cs.s));
-    CUDA_TRY(cudaStreamSynchronize(cs.s));
-    return download_split(p, x.p, n, re, im, cs.s);
+    return pafft_convolve_permfree_split_if(p, f, re, im, batch, nullptr, nullptr, nullptr);
 }
 
 pafft_status pafft_convolve_permfree_host_oop(pafft_plan_t p, pafft_filter_t f, const void* x_host, void* y_host,
@@ -1755,29 +1833,28 @@ pafft_status pafft_convolve_standard_split(pafft_plan_t p, const double* g_re, c
     if (!p) return fail(PAFFT_INVALID_ARGUMENT, "null plan");
     if (batch == 0) return PAFFT_OK;
     ST_TRY(set_device(p));
+    cudaStream_t st;
+    ST_TRY(call_stream(p->device, &st));
     const size_t n = p->total;
-    DevBuf g, x;
-    CUDA_TRY(cudaMalloc(&g.p, n * p->esize));
-    CUDA_TRY(cudaMalloc(&x.p, n * batch * p->esize));
-    CallStream cs;
-    CUDA_TRY(cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking));
-    ST_TRY(upload_split(p, g_re, g_im, n, g.p, cs.s));
-    ST_TRY(upload_split(p, re, im, n * batch, x.p, cs.s));
-    ST_TRY(pafft_convolve_standard(p, g.p, x.p, batch, cs.s));
-    CUDA_TRY(cudaStreamSynchronize(cs.s));
-    return download_split(p, x.p, n * batch, re, im, cs.s);
+    AsyncBuf g, x;
+    ST_TRY(async_alloc(p, g, n * p->esize, st));
+    ST_TRY(async_alloc(p, x, n * batch * p->esize, st));
+    ST_TRY(upload_split(p, g_re, g_im, n, g.p, st));
+    ST_TRY(upload_split(p, re, im, n * batch, x.p, st));
+    ST_TRY(pafft_convolve_standard(p, g.p, x.p, batch, st));
+    return download_split(p, x.p, n * batch, re, im, st);
 }
 
 pafft_status pafft_transform_split(pafft_plan_t p, int op, double* re, double* im, size_t batch) {
     if (!p) return fail(PAFFT_INVALID_ARGUMENT, "null plan");
     if (batch == 0) return PAFFT_OK;
+    if (op < 0 || op > 6) return fail(PAFFT_INVALID_ARGUMENT, "unknown transform op %d", op);
     ST_TRY(set_device(p));
+    cudaStream_t st;
+    ST_TRY(call_stream(p->device, &st));
     const size_t n = p->total * batch;
-    DevBuf x;
-    CUDA_TRY(cudaMalloc(&x.p, n * p->esize));
-    CallStream cs;
-    CUDA_TRY(cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking));
-    cudaStream_t st = cs.s;
+    AsyncBuf x;
+    ST_TRY(async_alloc(p, x, n * p->esize, st));
     ST_TRY(upload_split(p, re, im, n, x.p, st));
     switch (op) {
         case 0: ST_TRY(pafft_fft_forward(p, x.p, batch, st)); break;
@@ -1787,9 +1864,7 @@ pafft_status pafft_transform_split(pafft_plan_t p, int op, double* re, double* i
         case 4: ST_TRY(pafft_fft_transposed(p, x.p, batch, st)); break;
         case 5: ST_TRY(pafft_permute(p, x.p, batch, st)); break;
         case 6: ST_TRY(ladder_op(p, KIND_DIT_CONJ, false, 1.0, nullptr, x.p, batch, st)); break;
-        default: return fail(PAFFT_INVALID_ARGUMENT, "unknown transform op %d", op);
     }
-    CUDA_TRY(cudaStreamSynchronize(st));
     return download_split(p, x.p, n, re, im, st);
 }
 

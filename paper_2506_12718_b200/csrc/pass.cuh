@@ -219,8 +219,9 @@ template <typename T, typename FAC, int MAP, int WOVR = 0> struct TilePolicy {
     // complex value a thread holds (F_max of them) plus addressing
     static constexpr int REG_FLOOR = FAC::FMAX >= 25 ? 128 : (FAC::FMAX >= 16 ? 96 : (FAC::FMAX >= 9 ? 72 : 64));
     static constexpr int MINB_REG = 65536 / (((NT + 31) / 32 * 32) * REG_FLOOR);
+    // narrow-tile instances (WOVR) are sized for many small resident CTAs
     static constexpr int MAXB = NBUF == 1 ? (MINB_REG < PAFFT_SB_MAX_MINB ? MINB_REG : PAFFT_SB_MAX_MINB)
-                                          : PAFFT_MAX_MINB;
+                                          : (WOVR > 0 ? (MINB_REG < 16 ? MINB_REG : 16) : PAFFT_MAX_MINB);
     static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > MAXB ? MAXB : MINB_SMEM);
     static constexpr int NTB = NT;  // threads per block
 };
@@ -829,14 +830,16 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     }
 }
 
-template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP>
-__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
-                                  TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::MINB)
+// WOVR > 0: a narrow-tile instance (W = WOVR columns) for launches with few
+// tiles (batch-1 signals): more, smaller tiles so every SM gets several.
+template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP, int WOVR = 0>
+__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>::NTB,
+                                  TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>::MINB)
     pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap,
                 const __grid_constant__ CUtensorMap tmap_dst) {
     using V = cplx<T>;
     using FA = Fac<F0, F1, F2, F3>;
-    using Pol = TilePolicy<T, FA, MAP>;
+    using Pol = TilePolicy<T, FA, MAP, WOVR>;
     constexpr int R = FA::R, NS = FA::NS;
     constexpr int W = Pol::W;
     constexpr int SW = Pol::SW;
@@ -887,9 +890,18 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
                     const TileGeo g = tile_geo<R, W, STRIDED>(a, pend);
                     const long long nb = a.N / R, b0 = g.first % nb;
                     const long long nblk = b0 + g.nvalid <= nb ? g.nvalid : nb - b0;
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.ghat + b0 * R),
-                                 "r"((unsigned)(nblk * R * sizeof(V)))
-                                 : "memory");
+                    // the bulk prefetch needs a 16-byte aligned address and size:
+                    // fp32 blocks of odd R start 8 bytes off, so widen the range to
+                    // 16-byte bounds inside the filter
+                    const long long lo = (b0 * R * (long long)sizeof(V)) & ~15ll;
+                    const long long end = ((b0 + nblk) * R * (long long)sizeof(V) + 15) & ~15ll;
+                    const long long hi = end < ((a.N * (long long)sizeof(V)) & ~15ll) ? end
+                                                                                      : ((a.N * (long long)sizeof(V)) & ~15ll);
+                    if (hi > lo)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                         reinterpret_cast<const char*>(a.ghat) + lo),
+                                     "r"((unsigned)(hi - lo))
+                                     : "memory");
                 }
             }
         }

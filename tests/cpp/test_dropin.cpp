@@ -179,6 +179,66 @@ int main() {
         CHECK_THROWS_AS(convolve_permfree(z, f24, plan_create(Radix::r2, TensorShape{16, 16})), FilterPlanMismatch);
         CHECK_THROWS_AS(plan_create(std::vector<Radix>{Radix::r3, Radix::r2}, TensorShape{27, 27}), NotAPowerOfRadix);
     }
+    // PreparedFilter{ghat, key} is an aggregate whose ghat is the source of
+    // truth, as in the reference (convolution.hpp:9-12, convolution.cpp:49):
+    // a hand-built filter works, and an edit to ghat is honoured
+    {
+        const Plan plan = plan_create(Radix::r2, TensorShape{4});
+        ComplexBuffer delay(4);
+        delay.re[1] = 1.0;
+        const PreparedFilter built = prepare_filter(filter_from_impulse(delay, plan), plan);
+        const PreparedFilter by_hand{built.ghat, built.key};  // aggregate, no device copy
+        ComplexBuffer a = buf({1, 2, 3, 4}), b = a;
+        convolve_permfree(a, built, plan);
+        convolve_permfree(b, by_hand, plan);
+        CHECK(bitwise_equal(a, b) && max_diff(a, buf({4, 1, 2, 3})) < 1e-13);
+        PreparedFilter edited = built;  // a copy, then edit its spectrum: identity filter
+        for (std::size_t i = 0; i < 4; ++i) edited.ghat.set(i, 1.0);
+        ComplexBuffer c = buf({1, 2, 3, 4});
+        convolve_permfree(c, edited, plan);
+        CHECK(max_diff(c, buf({1, 2, 3, 4})) < 1e-13);
+        ComplexBuffer d = buf({1, 2, 3, 4});
+        convolve_permfree(d, built, plan);  // the shared original still delays
+        CHECK(max_diff(d, buf({4, 1, 2, 3})) < 1e-13);
+    }
+    // the same for a spectrum large enough that the byte check runs on a
+    // second thread, overlapped with the device call (commit-gated write-back)
+    {
+        const std::size_t n = std::size_t{1} << 16;
+        const Plan plan = plan_create(Radix::r4, TensorShape{n});
+        ComplexBuffer delay(n);
+        delay.re[1] = 1.0;
+        PreparedFilter f = prepare_filter(filter_from_impulse(delay, plan), plan);
+        const ComplexBuffer x = random_buffer(n, 95);
+        ComplexBuffer a = x;
+        convolve_permfree(a, f, plan);
+        CHECK(std::abs(a.re[1] - x.re[0]) < 1e-12 && std::abs(a.im[0] - x.im[n - 1]) < 1e-12);
+        for (std::size_t i = 0; i < n; ++i) f.ghat.set(i, 2.0);  // edit in place: 2 x identity
+        ComplexBuffer b = x;
+        convolve_permfree(b, f, plan);
+        double m = 0;
+        for (std::size_t i = 0; i < n; ++i) m = std::max(m, std::abs(b.get(i) - 2.0 * x.get(i)));
+        CHECK(m < 1e-12);
+        ComplexBuffer c = x;  // and again, from the rebuilt device copy
+        convolve_permfree(c, f, plan);
+        CHECK(bitwise_equal(b, c));
+    }
+    // C-order <-> vec repack (core.cpp:131-178 semantics): element (i0, i1, i2)
+    // of a C-order [2][3][4] tensor lands at vec offset i0 + 2 i1 + 6 i2
+    {
+        const TensorShape shape{2, 3, 4};
+        std::vector<std::complex<double>> vals(24);
+        for (std::size_t c = 0; c < 24; ++c) vals[c] = {double(c), -double(c)};
+        const ComplexBuffer v = buffer_from_tensor(vals, shape);
+        bool ok = true;
+        for (std::size_t i0 = 0; i0 < 2; ++i0)
+            for (std::size_t i1 = 0; i1 < 3; ++i1)
+                for (std::size_t i2 = 0; i2 < 4; ++i2)
+                    ok = ok && v.get(i0 + 2 * i1 + 6 * i2) == vals[i2 + 4 * i1 + 12 * i0];
+        CHECK(ok);
+        CHECK(tensor_from_buffer(v, shape) == vals);
+        CHECK_THROWS_AS(buffer_from_tensor(std::span<const std::complex<double>>(vals.data(), 23), shape), LengthMismatch);
+    }
     std::printf("dropin: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
 }
