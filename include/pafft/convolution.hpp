@@ -19,6 +19,10 @@
 #include <future>
 #include <memory>
 #include <mutex>
+#include <thread>
+#if defined(__linux__)
+#include <sched.h>
+#endif
 
 #include "core.hpp"
 
@@ -63,6 +67,16 @@ inline Fingerprint fingerprint(const ComplexBuffer& g) {
         f.b ^= f.b >> 27;
     }
     return f;
+}
+
+// Host CPUs this thread may run on (a caller pinned to one core, as the
+// reference's bench does, bench.cpp:52-59, gains nothing from a second thread).
+inline int cpus_available() {
+#if defined(__linux__)
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof set, &set) == 0) return CPU_COUNT(&set);
+#endif
+    return static_cast<int>(std::thread::hardware_concurrency());
 }
 
 // Device copy of a prepared spectrum plus the fingerprint of the host bytes
@@ -164,7 +178,7 @@ inline void convolve_permfree(ComplexBuffer& x, const PreparedFilter& filter, co
     }
     detail::DeviceFilter& dev = *filter.device;
     const std::shared_ptr<pafft_filter_s> cur = dev.current(plan);
-    if (cur && filter.ghat.size() >= (std::size_t{1} << 16)) {
+    if (cur && filter.ghat.size() >= (std::size_t{1} << 16) && detail::cpus_available() > 1) {
         // byte check of ghat on a second thread, overlapped with the upload and
         // the convolution; the result is written back only if it passes
         std::future<bool> same =

@@ -78,23 +78,20 @@ Registry& registry() {
         register_r4_f32(reg);
         register_r5_f32(reg);
         register_r8_f32(reg);
-        register_narrow_f64(reg);
-        register_narrow_f32(reg);
     });
     return reg;
 }
 
-const KernelEntry* find_kernel(int prec, int radix, int R, int kind, int map, int wovr = 0) {
+const KernelEntry* find_kernel(int prec, int radix, int R, int kind, int map) {
     for (const auto& e : registry())
-        if (e.prec == prec && e.radix == radix && e.R == R && e.kind == kind && e.map == map && e.wovr == wovr)
-            return &e;
+        if (e.prec == prec && e.radix == radix && e.R == R && e.kind == kind && e.map == map) return &e;
     return nullptr;
 }
 
 int max_stages_compiled(int prec, int radix, int kind, int map) {
     int best = 0;
     for (const auto& e : registry()) {
-        if (e.radix != radix || e.prec != prec || e.kind != kind || e.map != map || e.wovr) continue;
+        if (e.radix != radix || e.prec != prec || e.kind != kind || e.map != map) continue;
         int s = 0;
         for (int v = e.R; v > 1; v /= radix) ++s;
         best = std::max(best, s);
@@ -150,9 +147,6 @@ struct PassDesc {
     const void* ext_hi = nullptr;
     const void* tw[3] = {nullptr, nullptr, nullptr};
     const void* fn = nullptr;
-    // narrow-tile variant of a strided pass (fewer columns per tile), taken by
-    // launches whose default tiles would not fill the SMs (use_narrow)
-    std::shared_ptr<PassDesc> narrow;
 };
 
 struct Group {
@@ -420,19 +414,6 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     d.ext = d.L > 1;
     if (d.ext) ST_TRY(ext_table(p, d.K0, d));
     if (d.nsteps > 1) ST_TRY(int_table(p, d));
-    if (!d.contig) {
-        // narrow-tile variant (W = PAFFT_NARROW_W, default 4 fp64 / 8 fp32
-        // columns), when compiled for this stage group and narrower than the
-        // default tile
-        const int nw = env_int("PAFFT_NARROW_W", p->esize == 16 ? 4 : 8);
-        const KernelEntry* ne = nw > 0 ? find_kernel(p->prec, (int)radix, d.R, kind, MAP_STRIDED, nw) : nullptr;
-        if (ne && ne->W < d.W && ne->F0 == d.F[0] && ne->F1 == d.F[1] && ne->F2 == d.F[2] && ne->F3 == d.F[3]) {
-            auto nd = std::make_shared<PassDesc>(d);
-            nd->narrow.reset();
-            ST_TRY(bind_kernel(p, *ne, *nd));
-            d.narrow = nd;
-        }
-    }
     return PAFFT_OK;
 }
 
@@ -579,22 +560,8 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     return PAFFT_OK;
 }
 
-// A strided launch takes its narrow-tile variant when the default tiles are
-// fewer than two per resident CTA slot: one ragged wave in which most SMs hold
-// one or two large tiles and no tile pipelining happens (a batch-1 2^20
-// signal: 512 default tiles for 444 slots).  PAFFT_NARROW=0/1 forces it off/on.
-bool use_narrow(const PassDesc& d, const pafft_plan_s* p, size_t batch) {
-    if (!d.narrow) return false;
-    const int force = env_int("PAFFT_NARROW", -1);
-    if (force >= 0) return force != 0;
-    const long long per_signal = (long long)p->total / ((long long)d.R * d.C);
-    const long long tiles = per_signal * (long long)batch * ((d.C + d.W - 1) / d.W);
-    return tiles < 2 * d.max_ctas;
-}
-
-pafft_status launch(pafft_plan_t p, const PassDesc& d0, const void* src, void* dst, size_t batch,
+pafft_status launch(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
                     const void* ghat, const void* mul, double scale, cudaStream_t st, long long grid_cap = 0) {
-    const PassDesc& d = use_narrow(d0, p, batch) ? *d0.narrow : d0;
     return p->prec == 0 ? launch_t<double>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap)
                         : launch_t<float>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap);
 }
@@ -1207,11 +1174,6 @@ pafft_status pafft_plan_describe(pafft_plan_t p, char* buf, size_t len) {
                  kn[d.kind], d.axis, d.a, d.a + d.s, d.R, d.F[0], d.F[1], d.F[2], d.F[3], d.K0, d.L, d.C,
                  d.contig ? "contig" : "strided", d.W, d.NT, d.smem, d.ext);
         s += line;
-        if (d.narrow) {
-            snprintf(line, sizeof line, "  (few tiles: W=%d NT=%d smem=%zu slots=%lld)\n", d.narrow->W, d.narrow->NT,
-                     d.narrow->smem, d.narrow->max_ctas);
-            s += line;
-        }
     }
     if (buf && len) {
         strncpy(buf, s.c_str(), len - 1);

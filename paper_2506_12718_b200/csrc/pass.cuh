@@ -219,9 +219,8 @@ template <typename T, typename FAC, int MAP, int WOVR = 0> struct TilePolicy {
     // complex value a thread holds (F_max of them) plus addressing
     static constexpr int REG_FLOOR = FAC::FMAX >= 25 ? 128 : (FAC::FMAX >= 16 ? 96 : (FAC::FMAX >= 9 ? 72 : 64));
     static constexpr int MINB_REG = 65536 / (((NT + 31) / 32 * 32) * REG_FLOOR);
-    // narrow-tile instances (WOVR) are sized for many small resident CTAs
     static constexpr int MAXB = NBUF == 1 ? (MINB_REG < PAFFT_SB_MAX_MINB ? MINB_REG : PAFFT_SB_MAX_MINB)
-                                          : (WOVR > 0 ? (MINB_REG < 16 ? MINB_REG : 16) : PAFFT_MAX_MINB);
+                                          : PAFFT_MAX_MINB;
     static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > MAXB ? MAXB : MINB_SMEM);
     static constexpr int NTB = NT;  // threads per block
 };
@@ -830,16 +829,14 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     }
 }
 
-// WOVR > 0: a narrow-tile instance (W = WOVR columns) for launches with few
-// tiles (batch-1 signals): more, smaller tiles so every SM gets several.
-template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP, int WOVR = 0>
-__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>::NTB,
-                                  TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>::MINB)
+template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP>
+__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
+                                  TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::MINB)
     pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap,
                 const __grid_constant__ CUtensorMap tmap_dst) {
     using V = cplx<T>;
     using FA = Fac<F0, F1, F2, F3>;
-    using Pol = TilePolicy<T, FA, MAP, WOVR>;
+    using Pol = TilePolicy<T, FA, MAP>;
     constexpr int R = FA::R, NS = FA::NS;
     constexpr int W = Pol::W;
     constexpr int SW = Pol::SW;

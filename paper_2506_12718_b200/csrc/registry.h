@@ -15,7 +15,6 @@ struct KernelEntry {
     int map;    // PassMap
     int W, NT, smem;  // compile-time tile policy of this instance
     const void* fn;
-    int wovr = 0;     // > 0: narrow-tile variant (W forced) for few-tile launches
 };
 
 using Registry = std::vector<KernelEntry>;
@@ -30,8 +29,7 @@ void register_r3_f32(Registry&);
 void register_r4_f32(Registry&);
 void register_r5_f32(Registry&);
 void register_r8_f32(Registry&);
-void register_narrow_f64(Registry&);
-void register_narrow_f32(Registry&);
+
 
 }  // namespace pafft_b200
 
