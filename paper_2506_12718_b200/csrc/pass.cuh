@@ -71,6 +71,7 @@
 #define PAFFT_SB_MAX_MINB 8
 #endif
 
+
 // PAFFT_DEBUG builds (tools/debug_build.sh) check tile geometry and
 // shared-memory indices on the device; release builds compile them out.
 #ifdef PAFFT_DEBUG
@@ -829,6 +830,33 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     }
 }
 
+// L2 prefetch of bytes [lo, hi) of a buffer (one thread): the bulk prefetch
+// needs a 16-byte aligned address and size, so the range is widened to 16-byte
+// bounds and clipped to `limit` (fp32 blocks of odd length start 8 bytes off).
+__device__ __forceinline__ void l2_prefetch_range(const void* base, long long lo, long long hi, long long limit) {
+    lo &= ~15ll;
+    hi = (hi + 15) & ~15ll;
+    if (hi > (limit & ~15ll)) hi = limit & ~15ll;
+    if (hi > lo)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(base) + lo),
+                     "r"((unsigned)(hi - lo))
+                     : "memory");
+}
+
+// The filter blocks a CONV tile will multiply by, into L2 ahead of the
+// multiply: measured on B200 config 4 (256 MiB filter) CONV -9%, config 2
+// (24 MiB) -2%; a filter of a few MiB stays in L2 anyway (size floor).
+template <int R, int W, typename T>
+__device__ __forceinline__ void prefetch_filter_blocks(const PassArgs<T>& a, long long tile) {
+    using V = cplx<T>;
+    if (a.N * (long long)sizeof(V) < (8ll << 20)) return;
+    const TileGeo g = tile_geo<R, W, false>(a, tile);
+    const long long nb = a.N / R, b0 = g.first % nb;
+    const long long nblk = b0 + g.nvalid <= nb ? g.nvalid : nb - b0;
+    l2_prefetch_range(a.ghat, b0 * R * (long long)sizeof(V), (b0 + nblk) * R * (long long)sizeof(V),
+                      a.N * (long long)sizeof(V));
+}
+
 template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP>
 __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
                                   TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::MINB)
@@ -877,29 +905,10 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
             __syncwarp();
             fence_proxy_async();
             stage_tile<R, W, SW, STRIDED>(a, &tmap, pend, pbuf, pbar, lane);
+            // (the instruction-cache-bound 25-point kernels, config 5, lose ~1%
+            // to the extra code, so they skip it)
             if constexpr (KIND == KIND_CONV && PAFFT_GHAT_PF && FA::FMAX < 25) {
-                // the staged tile's filter blocks into L2 ahead of the multiply:
-                // measured on B200 config 4 (256 MiB filter) CONV -9%, config 2
-                // (24 MiB) -2%; a filter of a few MiB stays in L2 anyway (size
-                // floor), and the instruction-cache-bound 25-point kernels
-                // (config 5) lose ~1% to the extra code, so they skip it
-                if (lane == 0 && a.N * (long long)sizeof(V) >= (8ll << 20)) {
-                    const TileGeo g = tile_geo<R, W, STRIDED>(a, pend);
-                    const long long nb = a.N / R, b0 = g.first % nb;
-                    const long long nblk = b0 + g.nvalid <= nb ? g.nvalid : nb - b0;
-                    // the bulk prefetch needs a 16-byte aligned address and size:
-                    // fp32 blocks of odd R start 8 bytes off, so widen the range to
-                    // 16-byte bounds inside the filter
-                    const long long lo = (b0 * R * (long long)sizeof(V)) & ~15ll;
-                    const long long end = ((b0 + nblk) * R * (long long)sizeof(V) + 15) & ~15ll;
-                    const long long hi = end < ((a.N * (long long)sizeof(V)) & ~15ll) ? end
-                                                                                      : ((a.N * (long long)sizeof(V)) & ~15ll);
-                    if (hi > lo)
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                                         reinterpret_cast<const char*>(a.ghat) + lo),
-                                     "r"((unsigned)(hi - lo))
-                                     : "memory");
-                }
+                if (lane == 0) prefetch_filter_blocks<R, W>(a, pend);
             }
         }
         pend = -1;
