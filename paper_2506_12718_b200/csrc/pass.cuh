@@ -137,6 +137,17 @@ template <int RADIX, int P> __host__ __device__ constexpr int revd(int k) {
     return o;
 }
 
+// The same at run time (power-of-radix P, small: unrolled).
+template <int RADIX, int P> __device__ __forceinline__ int revd_rt_dev(int k) {
+    int o = 0;
+#pragma unroll
+    for (int p = 1; p < P; p *= RADIX) {
+        o = o * RADIX + k % RADIX;
+        k /= RADIX;
+    }
+    return o;
+}
+
 // Codelet split R = F0 * F1 * F2 * F3 (trailing 1s unused).  Step i works on
 // digit i of the row index m = sum_i m_i wt(i), wt(i) = F_{i+1} ... F_last:
 // groups are all combinations of the other digits, G(i) = R / F_i of them.
@@ -467,6 +478,43 @@ template <int F, int P, int Q, int S, typename V> __device__ __forceinline__ voi
     });
 }
 
+// Lane-rotated access for strided tiles of narrow rows.  In a step with
+// Q = 1 a group's F rows are consecutive, so with rows of 16*SW < 128 bytes the
+// GQ = 128 / (16*SW) groups of a quarter-warp read and write rows that are all
+// F rows apart -- the same banks, a GQ-way conflict (config 3's 32-byte rows:
+// 4-way on every access of its last step).  Each group instead walks its rows
+// starting at a lane-dependent offset (q for natural row order, q * F / GQ for
+// digit-reversed order, which spreads the rows over all banks), and the
+// registers are rotated back with a log2(GQ)-stage select network.
+#ifndef PAFFT_ROT
+#define PAFFT_ROT 1
+#endif
+// z[j] = t[(j - s) mod F] for s = q * unit, q < 2^BITS (barrel shifter of selects)
+template <int F, int UNIT, int BITS, typename V> __device__ __forceinline__ void rotate_right(V (&z)[F], int q) {
+    static_for<0, BITS>([&](auto bc) {
+        constexpr int b = decltype(bc)::value;
+        constexpr int sh = (UNIT << b) % F;
+        const bool on = (q >> b) & 1;
+        V u[F];
+#pragma unroll
+        for (int j = 0; j < F; ++j) u[j] = on ? z[(j - sh + F) % F] : z[j];
+#pragma unroll
+        for (int j = 0; j < F; ++j) z[j] = u[j];
+    });
+}
+template <int F, int UNIT, int BITS, typename V> __device__ __forceinline__ void rotate_left(V (&z)[F], int q) {
+    static_for<0, BITS>([&](auto bc) {
+        constexpr int b = decltype(bc)::value;
+        constexpr int sh = (UNIT << b) % F;
+        const bool on = (q >> b) & 1;
+        V u[F];
+#pragma unroll
+        for (int j = 0; j < F; ++j) u[j] = on ? z[(j + sh) % F] : z[j];
+#pragma unroll
+        for (int j = 0; j < F; ++j) z[j] = u[j];
+    });
+}
+
 // DIT epilogue of the transforms and the standard-order comparator (natural-
 // order multiplier of period N, then a scale), kept out of line.
 #ifndef PAFFT_EPI_CALL
@@ -567,6 +615,10 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     // Chebyshev twiddle powers for 16-point steps (codelets.cuh) where enough
     // warps hide its longer chain: contiguous tiles of >= 256 threads
     constexpr bool CHEB16 = !STRIDED && Pol::NT >= 256;
+    // lane-rotated Q = 1 steps (PAFFT_ROT): fp64 strided rows narrower than 128 B
+    constexpr int GQ = (STRIDED && !SHIFT && SW * (int)sizeof(V) < 128) ? 128 / (SW * (int)sizeof(V)) : 1;
+    constexpr int GQB = GQ >= 8 ? 3 : GQ >= 4 ? 2 : GQ >= 2 ? 1 : 0;
+    constexpr bool ROT = PAFFT_ROT && GQ > 1 && (FL & (FL - 1)) == 0 && FL >= GQ && (32 % W == 0);
     (void)BUFE;
     (void)buf_end;
     const int warp = t >> 5, lane = t & 31;
@@ -575,6 +627,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     // W-wide row segments, conflict-free smem rows); CONTIG: group fastest.
     const int c = STRIDED ? t % W : t / GMIN;
     const int gt = STRIDED ? t / W : t % GMIN;
+    const int rq = ROT ? gt % GQ : 0;  // this thread's rotation (the group's place in its quarter-warp)
     constexpr int SS = STRIDED ? SW : 1;  // shared stride between consecutive rows
     const long long rs = STRIDED ? (long long)a.C : 1;  // global row stride
     const TileGeo geo = tile_geo<R, W, STRIDED>(a, tile);
@@ -669,8 +722,15 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                 const int hi = g / QI, lo = g - (g / QI) * QI;
                 const int sb = hi * PI + lo;
                 V z[FI];
+                if constexpr (ROT && KIND == KIND_DIF && I == NS - 1) {
+                    // rows sb + (m + q) mod F, then rotate back
 #pragma unroll
-                for (int m = 0; m < FI; ++m) z[m] = sref(sb + m * QI);
+                    for (int m = 0; m < FI; ++m) z[m] = sref(sb + ((m + rq) & (FI - 1)));
+                    rotate_right<FI, 1, GQB>(z, rq);
+                } else {
+#pragma unroll
+                    for (int m = 0; m < FI; ++m) z[m] = sref(sb + m * QI);
+                }
                 dft<FI, 1>(z);
                 if constexpr (I < NS - 1) {
                     // w_{P_I}^{k lo}: powers of tw[I][Q_I + lo] = w_{P_I}^{lo}
@@ -733,9 +793,17 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
             if constexpr (WSCAT) __syncwarp();
             else __syncthreads();
 #pragma unroll
-            for (int j = 0; j < (act ? NGL : 0); ++j)
+            for (int j = 0; j < (act ? NGL : 0); ++j) {
+                if constexpr (ROT) {
+                    // frequency (k + q F/GQ) mod F at instruction k: digit-reversed rows spread over the banks
+                    rotate_left<FL, FL / GQ, GQB>(zl[j], rq);
 #pragma unroll
-                for (int k = 0; k < FL; ++k) sref(pl[j] + revd<RADIX, FL>(k)) = zl[j][k];
+                    for (int k = 0; k < FL; ++k) sref(pl[j] + revd_rt_dev<RADIX, FL>((k + rq * (FL / GQ)) & (FL - 1))) = zl[j][k];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < FL; ++k) sref(pl[j] + revd<RADIX, FL>(k)) = zl[j][k];
+                }
+            }
         } else if (ok) {
 #pragma unroll
             for (int j = 0; j < NGL; ++j)
@@ -762,8 +830,16 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                     const int hi = g / QI, lo = g - (g / QI) * QI;
                     const int sb = hi * PI + lo;
                     V z[FI];
+                    constexpr bool RL = ROT && FIRST && I == NS - 1;  // rotated Q = 1 step
+                    if constexpr (RL) {
 #pragma unroll
-                    for (int k = 0; k < FI; ++k) z[k] = sref(sb + (FIRST ? revd<RADIX, FI>(k) : k) * QI);
+                        for (int k = 0; k < FI; ++k)
+                            z[k] = sref(sb + revd_rt_dev<RADIX, FI>((k + rq * (FI / GQ)) & (FI - 1)));
+                        rotate_right<FI, FI / GQ, GQB>(z, rq);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < FI; ++k) z[k] = sref(sb + (FIRST ? revd<RADIX, FI>(k) : k) * QI);
+                    }
                     if constexpr (FIRST && I == NS - 1) {
                         // pre-twiddle w_K0^{+-jj k} on the first DIT step
                         if (a.ext && ok) {
@@ -790,8 +866,14 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                     }
                     dft<FI, S>(z);
                     if constexpr (I > 0) {
+                        if constexpr (RL) {
+                            rotate_left<FI, 1, GQB>(z, rq);
 #pragma unroll
-                        for (int m = 0; m < FI; ++m) sref(sb + m * QI) = z[m];
+                            for (int m = 0; m < FI; ++m) sref(sb + ((m + rq) & (FI - 1))) = z[m];
+                        } else {
+#pragma unroll
+                            for (int m = 0; m < FI; ++m) sref(sb + m * QI) = z[m];
+                        }
                     } else {
                         // final spatial rows m * Q_0 + lo (hi == 0), epilogue in registers
                         V* gp = gdst + (long long)lo * rs;
