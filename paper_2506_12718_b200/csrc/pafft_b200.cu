@@ -891,12 +891,21 @@ pafft_status passes_permfree(pafft_plan_t p, std::vector<PassDesc>& out) {
     return PAFFT_OK;
 }
 
-// A (kind DIT_FWD) / A-bar (DIT_CONJ): reverse group order; A^T (DIF): group order.
+// Ladders over every mode in the reference's mode order (butterfly_tensor,
+// butterfly.cpp:423-466: mode 0 first, ascending), so a tensor ladder is
+// bitwise the 1-D ladder applied line by line (test_butterfly.cpp:198-215).
+// A (DIT_FWD) / A-bar (DIT_CONJ): reverse group order (axis 0 first, its
+// stage groups descending).  A^T (DIF): axes ascending, each axis's stage
+// groups ascending (the permutation-free schedule keeps its own order: there
+// axis 0's contiguous group must come last to merge with the filter).
 pafft_status passes_ladder(pafft_plan_t p, int kind, std::vector<PassDesc>& out) {
     out.clear();
-    const size_t ng = p->groups.size();
-    for (size_t i = 0; i < ng; ++i) {
-        const Group& g = kind == KIND_DIF ? p->groups[i] : p->groups[ng - 1 - i];
+    std::vector<Group> order(p->groups.begin(), p->groups.end());
+    if (kind == KIND_DIF)
+        std::stable_sort(order.begin(), order.end(), [](const Group& x, const Group& y) { return x.axis < y.axis; });
+    else
+        std::reverse(order.begin(), order.end());
+    for (const Group& g : order) {
         PassDesc d;
         ST_TRY(make_pass(p, g, kind, d));
         out.push_back(d);
