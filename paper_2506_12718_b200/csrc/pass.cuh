@@ -643,6 +643,13 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     const int codd = SHIFT && !a.use_tmap ? (a.C & 1) : 0;
     const int b0 = SHIFT && !a.use_tmap ? (int)(geo.base & 1) : 0;
     const int swx = a.swz;  // 0/1
+    // CONV tiles in the 128B-swizzled layout with a 16-point last step: the
+    // group bases gt*16 map a quarter-warp's 8 groups onto 4 swizzle phases
+    // (2-way conflicts); groups with bit 2 of gt set walk their 16 rows from
+    // the upper half (m ^ 8), which separates the pairs (PAFFT_ROT)
+    constexpr bool ROTC = PAFFT_ROT && !STRIDED && KIND == KIND_CONV && sizeof(V) == 16 &&
+                          (RADIX == 2 || RADIX == 4 || RADIX == 8) && FL == 16;
+    const int rqc = ROTC ? (swx & (gt >> 2) & 1) : 0;
     auto sref = [&](int row) -> V& {
         PAFFT_DASSERT(row >= 0 && row < R);
         if constexpr (!STRIDED && (RADIX == 2 || RADIX == 4 || RADIX == 8)) {
@@ -727,6 +734,10 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
 #pragma unroll
                     for (int m = 0; m < FI; ++m) z[m] = sref(sb + ((m + rq) & (FI - 1)));
                     rotate_right<FI, 1, GQB>(z, rq);
+                } else if constexpr (ROTC && I == NS - 1) {
+#pragma unroll
+                    for (int m = 0; m < FI; ++m) z[m] = sref(sb + (m ^ (rqc << 3)));
+                    rotate_right<FI, 8, 1>(z, rqc);
                 } else {
 #pragma unroll
                     for (int m = 0; m < FI; ++m) z[m] = sref(sb + m * QI);
@@ -779,8 +790,14 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
                                 for (int m = 0; m < FI; ++m) gdst[(long long)m * rs] = z[m];
                             }
                         } else {
+                            if constexpr (ROTC) {
+                                rotate_left<FI, 8, 1>(z, rqc);
 #pragma unroll
-                            for (int m = 0; m < FI; ++m) sref(sb + m) = z[m];
+                                for (int m = 0; m < FI; ++m) sref(sb + (m ^ (rqc << 3))) = z[m];
+                            } else {
+#pragma unroll
+                                for (int m = 0; m < FI; ++m) sref(sb + m) = z[m];
+                            }
                         }
                     }
                 }
