@@ -343,10 +343,20 @@ class Gpu:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(self.local)
+        # PAFFT_BENCH_BACKEND=gloo: a plumbing check of the multi-rank flow
+        # (partition, filter broadcast, max over ranks, rank-0 line) with ranks
+        # that may share a GPU (device = local rank mod device count); its
+        # timings are not a measurement.  Default: NCCL, one GPU per rank.
+        backend = os.environ.get("PAFFT_BENCH_BACKEND", "nccl")
+        self.device_index = self.local % max(1, torch.cuda.device_count()) if backend != "nccl" else self.local
+        torch.cuda.set_device(self.device_index)
         if self.world > 1:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
-        self.dev = torch.device("cuda", self.local)
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device_index))
+            else:
+                dist.init_process_group(backend)
+        self.dev = torch.device("cuda", self.device_index)
+        self.local = self.device_index
         self.gpu_index = self.local
         cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
         if cvd:
