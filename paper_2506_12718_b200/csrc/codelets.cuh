@@ -237,11 +237,18 @@ template <int P, int S, typename V> __device__ __forceinline__ void dft(V (&z)[P
 #ifndef PAFFT_CHEB_MIN
 #define PAFFT_CHEB_MIN 25
 #endif
+// fp32 twiddle powers by binary powering only: the Chebyshev recurrence's
+// error growth (~k cot(theta) ulps) costs 7x accuracy in fp32 (config 5 fp32:
+// 7.0e-6 relative L2 against the 1e-5 bar, 1.0e-6 with binary powers;
+// configs 1/3/4 fp32 3x) for 2% of config 5 fp32 speed (config 1 fp32 +2%)
+#ifndef PAFFT_CHEB_F32
+#define PAFFT_CHEB_F32 0
+#endif
 template <int F, int S, bool CHEB16 = false, typename V>
 __device__ __forceinline__ void twiddle_powers(V (&z)[F], V w) {
     if constexpr (F > 1) {
         if constexpr (S < 0) w.y = -w.y;
-        if constexpr (F >= PAFFT_CHEB_MIN || (CHEB16 && F >= 16)) {
+        if constexpr ((F >= PAFFT_CHEB_MIN || (CHEB16 && F >= 16)) && (PAFFT_CHEB_F32 || sizeof(w.x) == 8)) {
             using T = decltype(w.x);
             const T c2 = w.x + w.x;
             V pm{(T)1, (T)0}, pc = w;
