@@ -11,6 +11,9 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PAFFT_LIB") or os.path.join(HERE, "libpafft_b200.so")  # PAFFT_LIB: A/B builds
+if not os.path.isabs(LIB_PATH) and not os.path.exists(LIB_PATH):
+    # a relative PAFFT_LIB names a file under the repo root (e.g. ab/lib<tag>.so)
+    LIB_PATH = os.path.join(os.path.dirname(HERE), LIB_PATH)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
