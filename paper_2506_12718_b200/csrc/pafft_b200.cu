@@ -78,20 +78,22 @@ Registry& registry() {
         register_r4_f32(reg);
         register_r5_f32(reg);
         register_r8_f32(reg);
+        register_wide_f64(reg);
     });
     return reg;
 }
 
-const KernelEntry* find_kernel(int prec, int radix, int R, int kind, int map) {
+const KernelEntry* find_kernel(int prec, int radix, int R, int kind, int map, int wide = 0) {
     for (const auto& e : registry())
-        if (e.prec == prec && e.radix == radix && e.R == R && e.kind == kind && e.map == map) return &e;
+        if (e.prec == prec && e.radix == radix && e.R == R && e.kind == kind && e.map == map && e.wide == wide)
+            return &e;
     return nullptr;
 }
 
 int max_stages_compiled(int prec, int radix, int kind, int map) {
     int best = 0;
     for (const auto& e : registry()) {
-        if (e.radix != radix || e.prec != prec || e.kind != kind || e.map != map) continue;
+        if (e.radix != radix || e.prec != prec || e.kind != kind || e.map != map || e.wide) continue;
         int s = 0;
         for (int v = e.R; v > 1; v /= radix) ++s;
         best = std::max(best, s);
@@ -147,6 +149,9 @@ struct PassDesc {
     const void* ext_hi = nullptr;
     const void* tw[3] = {nullptr, nullptr, nullptr};
     const void* fn = nullptr;
+    // wide strided variant (16 columns, 256-byte rows), taken by launches
+    // with many tiles (use_wide)
+    std::shared_ptr<PassDesc> wide;
 };
 
 struct Group {
@@ -414,6 +419,16 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     d.ext = d.L > 1;
     if (d.ext) ST_TRY(ext_table(p, d.K0, d));
     if (d.nsteps > 1) ST_TRY(int_table(p, d));
+    if (!d.contig) {
+        const KernelEntry* we = find_kernel(p->prec, (int)radix, d.R, kind, MAP_STRIDED, 1);
+        if (we && we->W > d.W && we->F0 == d.F[0] && we->F1 == d.F[1] && we->F2 == d.F[2] && we->F3 == d.F[3] &&
+            env_int("PAFFT_WIDE", 1)) {
+            auto wd = std::make_shared<PassDesc>(d);
+            wd->wide.reset();
+            ST_TRY(bind_kernel(p, *we, *wd));
+            d.wide = wd;
+        }
+    }
     return PAFFT_OK;
 }
 
@@ -560,8 +575,19 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     return PAFFT_OK;
 }
 
-pafft_status launch(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
+// A strided launch takes its wide variant when that still gives at least four
+// tiles per resident CTA slot (a full pipeline on every SM); batch-1 signals
+// keep the 8-column tiles (config 1: 256 wide tiles for 148 slots).
+bool use_wide(const PassDesc& d, const pafft_plan_s* p, size_t batch) {
+    if (!d.wide) return false;
+    const long long per_signal = (long long)p->total / ((long long)d.R * d.C);
+    const long long tiles = per_signal * (long long)batch * ((d.C + d.wide->W - 1) / d.wide->W);
+    return tiles >= 4 * d.wide->max_ctas;
+}
+
+pafft_status launch(pafft_plan_t p, const PassDesc& d0, const void* src, void* dst, size_t batch,
                     const void* ghat, const void* mul, double scale, cudaStream_t st, long long grid_cap = 0) {
+    const PassDesc& d = use_wide(d0, p, batch) ? *d0.wide : d0;
     return p->prec == 0 ? launch_t<double>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap)
                         : launch_t<float>(p, d, src, dst, batch, ghat, mul, scale, st, grid_cap);
 }
@@ -1183,6 +1209,10 @@ pafft_status pafft_plan_describe(pafft_plan_t p, char* buf, size_t len) {
                  kn[d.kind], d.axis, d.a, d.a + d.s, d.R, d.F[0], d.F[1], d.F[2], d.F[3], d.K0, d.L, d.C,
                  d.contig ? "contig" : "strided", d.W, d.NT, d.smem, d.ext);
         s += line;
+        if (d.wide) {
+            snprintf(line, sizeof line, "  (many tiles: W=%d NT=%d smem=%zu)\n", d.wide->W, d.wide->NT, d.wide->smem);
+            s += line;
+        }
     }
     if (buf && len) {
         strncpy(buf, s.c_str(), len - 1);

@@ -956,14 +956,16 @@ __device__ __forceinline__ void prefetch_filter_blocks(const PassArgs<T>& a, lon
                       a.N * (long long)sizeof(V));
 }
 
-template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP>
-__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::NTB,
-                                  TilePolicy<T, Fac<F0, F1, F2, F3>, MAP>::MINB)
+// WOVR > 0: an instance with W = WOVR columns per tile (the wide strided
+// variants of inst/inst_wide.cu, taken by launches with many tiles).
+template <typename T, int RADIX, int F0, int F1, int F2, int F3, int KIND, int MAP, int WOVR = 0>
+__global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>::NTB,
+                                  TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>::MINB)
     pass_kernel(const PassArgs<T> a, const __grid_constant__ CUtensorMap tmap,
                 const __grid_constant__ CUtensorMap tmap_dst) {
     using V = cplx<T>;
     using FA = Fac<F0, F1, F2, F3>;
-    using Pol = TilePolicy<T, FA, MAP>;
+    using Pol = TilePolicy<T, FA, MAP, WOVR>;
     constexpr int R = FA::R, NS = FA::NS;
     constexpr int W = Pol::W;
     constexpr int SW = Pol::SW;

@@ -15,6 +15,7 @@ struct KernelEntry {
     int map;    // PassMap
     int W, NT, smem;  // compile-time tile policy of this instance
     const void* fn;
+    int wide = 0;     // 1: wide strided variant (more columns per tile) for launches with many tiles
 };
 
 using Registry = std::vector<KernelEntry>;
@@ -29,6 +30,7 @@ void register_r3_f32(Registry&);
 void register_r4_f32(Registry&);
 void register_r5_f32(Registry&);
 void register_r8_f32(Registry&);
+void register_wide_f64(Registry&);
 
 
 }  // namespace pafft_b200
