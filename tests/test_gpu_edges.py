@@ -118,3 +118,25 @@ def test_maximum_sizes_properties(pf, torch, radix, dims):
     r2 = pf.convolve_permfree_out(x2, x2, f, plan)  # in place
     torch.cuda.synchronize()
     assert float(torch.linalg.vector_norm(lhs - (a * r1 + b * r2)) / torch.linalg.vector_norm(lhs)) <= 1e-12
+
+
+@pytest.mark.parametrize("radix,dims,batch", [(4, [256, 256, 16], 2), (2, [64, 256, 8], 4), (8, [8, 64, 64], 3)])
+def test_wide_strided_tiles_are_bitwise_the_narrow_ones(pf, torch, monkeypatch, radix, dims, batch):
+    """Launches with many tiles take the 16-column strided instances
+    (inst_wide.cu, use_wide); per column they do the same arithmetic as the
+    8-column ones, so the convolution is bitwise identical (PAFFT_WIDE=0 at
+    plan creation disables them)."""
+    import numpy as np
+    n = int(np.prod(dims))
+    rng = np.random.default_rng(11)
+    x = torch.from_numpy(rng.standard_normal((batch, n)) + 1j * rng.standard_normal((batch, n))).cuda()
+    h = torch.from_numpy(rng.standard_normal(n) + 1j * rng.standard_normal(n)).cuda()
+    wide = pf.Plan(radix, dims)
+    monkeypatch.setenv("PAFFT_WIDE", "0")
+    narrow = pf.Plan(radix, dims)
+    monkeypatch.delenv("PAFFT_WIDE")
+    assert "many tiles" in wide.describe() and "many tiles" not in narrow.describe()
+    yw = pf.convolve_permfree_out(x, torch.empty_like(x), pf.prepare_filter_from_impulse(h, wide), wide)
+    yn = pf.convolve_permfree_out(x, torch.empty_like(x), pf.prepare_filter_from_impulse(h, narrow), narrow)
+    torch.cuda.synchronize()
+    assert torch.equal(yw, yn)
