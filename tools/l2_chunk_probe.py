@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--chunks", default="64,32,16,8,4,3,2,1")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--graph", action="store_true")
+    ap.add_argument("--streams", default="1", help="comma list: chunks are issued round-robin on this many streams")
     a = ap.parse_args()
     cfg = workload.get_config(a.config, a.precision)
     B = a.batch or cfg.batch
@@ -38,11 +39,24 @@ def main():
     y = torch.empty_like(x)
     s = torch.cuda.current_stream()
     print(f"config {a.config} {a.precision} batch {B} signal {N * x.element_size() / 2**20:.1f} MiB", flush=True)
-    for c in [int(v) for v in a.chunks.split(",")]:
+    side = [torch.cuda.Stream() for _ in range(8)]
+    for c, ns in [(int(v), int(w)) for w in a.streams.split(",") for v in a.chunks.split(",")]:
         def run():
-            for b0 in range(0, B, c):
+            s = torch.cuda.current_stream()  # the capture stream under --graph
+            if ns > 1:
+                ev = torch.cuda.Event()
+                ev.record(s)
+                for q in side[:ns]:
+                    q.wait_event(ev)
+            for i, b0 in enumerate(range(0, B, c)):
                 b1 = min(B, b0 + c)
-                pf.convolve_permfree_out(x[b0:b1], y[b0:b1], filt, plan, stream=s)
+                q = s if ns == 1 else side[i % ns]
+                pf.convolve_permfree_out(x[b0:b1], y[b0:b1], filt, plan, stream=q)
+            if ns > 1:
+                for q in side[:ns]:
+                    e = torch.cuda.Event()
+                    e.record(q)
+                    s.wait_event(e)
         for _ in range(3):
             run()
         torch.cuda.synchronize()
@@ -57,14 +71,14 @@ def main():
         for _ in range(a.reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
-            e0.record(s)
+            e0.record(torch.cuda.current_stream())
             fn()
-            e1.record(s)
+            e1.record(torch.cuda.current_stream())
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         ts.sort()
         ms = ts[len(ts) // 2]
-        print(f"chunk {c:5d}: {ms:8.3f} ms per {B} convs  {B / ms * 1e3:10.1f} conv/s  "
+        print(f"streams {ns} chunk {c:5d}: {ms:8.3f} ms per {B} convs  {B / ms * 1e3:10.1f} conv/s  "
               f"(chunk working set {c * N * x.element_size() / 2**20:.0f} MiB + filter)", flush=True)
 
 
