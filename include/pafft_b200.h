@@ -208,6 +208,9 @@ uint64_t pafft_permutation_pass_count(void);
 void pafft_reset_permutation_pass_count(void);
 /* Kernel launches issued by this library on this thread (all kinds). */
 uint64_t pafft_kernel_launch_count(void);
+/* Pass launches on this thread whose tiles were handed out dynamically (a
+ * per-stream counter) instead of in the static round-robin order. */
+uint64_t pafft_dynamic_launch_count(void);
 
 /* ------------------------------------------------------- workload gen --
  * SplitMix64 (bench.cpp:22-42), interleaved output, n complex elements.

@@ -31,7 +31,7 @@ __all__ = [
     "filter_from_impulse", "prepare_filter", "fft_transposed", "permute",
     "Error", "NotAPowerOfRadix", "EmptyShape", "LengthMismatch", "ShapeMismatch", "FilterPlanMismatch",
     "IndexOutOfRange", "CudaError", "NoDevice",
-    "permutation_pass_count", "reset_permutation_pass_count", "kernel_launch_count",
+    "permutation_pass_count", "reset_permutation_pass_count", "kernel_launch_count", "dynamic_launch_count",
     "F64", "F32",
 ]
 
@@ -340,6 +340,10 @@ def reset_permutation_pass_count():
 
 def kernel_launch_count():
     return lib.pafft_kernel_launch_count()
+
+
+def dynamic_launch_count():
+    return lib.pafft_dynamic_launch_count()
 
 
 # ============================================================= device API

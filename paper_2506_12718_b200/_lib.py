@@ -77,6 +77,7 @@ _SIGS = {
     "pafft_permutation_pass_count": ([], C.c_uint64),
     "pafft_reset_permutation_pass_count": ([], None),
     "pafft_kernel_launch_count": ([], C.c_uint64),
+    "pafft_dynamic_launch_count": ([], C.c_uint64),
     "pafft_fill_uniform": ([C.c_uint64, _sz, _dp], None),
     "pafft_fill_normal": ([C.c_uint64, _sz, _dp], None),
 }

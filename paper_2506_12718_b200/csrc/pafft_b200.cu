@@ -38,6 +38,7 @@ thread_local std::string g_err;
 thread_local size_t g_err_dim = 0, g_err_extent = 0;
 thread_local uint64_t g_perm_passes = 0;
 thread_local uint64_t g_launches = 0;
+thread_local uint64_t g_dynamic_launches = 0;  // pass launches that handed tiles out dynamically
 
 pafft_status fail(pafft_status st, const char* fmt, ...) {
     char buf[512];
@@ -141,6 +142,7 @@ struct PassDesc {
     int contig = 0, W = 1, NT = 32;
     size_t smem = 0;
     long long max_ctas = 1;
+    int occ = 1;  // resident CTAs per SM
     int use_tmap = 0, rb = 0, sw = 0;  // STRIDED tensor-map staging
     int swz = 0, swz_b1 = 0;           // CONTIG 128B-swizzled staging (power-of-two radix)
     int ext = 0;
@@ -369,6 +371,7 @@ pafft_status bind_kernel(pafft_plan_t p, const KernelEntry& ke, PassDesc& d) {
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
     if (occ < 1) return fail(PAFFT_CUDA_ERROR, "pass kernel R=%d cannot be resident (smem %zu)", d.R, d.smem);
     d.max_ctas = (long long)occ * sms;
+    d.occ = occ;
     if (!d.contig) d.sw = p->esize == 8 ? d.W + 2 : d.W;
     return PAFFT_OK;
 }
@@ -515,6 +518,47 @@ pafft_status tensor_map_swz(pafft_plan_t p, const PassDesc& d, const void* src, 
     return PAFFT_OK;
 }
 
+// Dynamic tile order (pass.cuh): a {next tile, retired CTAs} counter pair per
+// (device, stream).  Launches on one stream run one after another and each
+// leaves its pair zeroed, so the pair needs no host-side reset; streams run
+// concurrently, so each has its own.  Launches that cannot be tied to one
+// stream keep the static order: a capturing stream (the graph may replay on
+// any stream, next to other graphs captured on the same one) and the
+// per-thread default stream (one handle, a different stream per thread).
+unsigned* tile_counters(int device, cudaStream_t st) {
+    if (st == cudaStreamPerThread) return nullptr;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (st == cudaStreamLegacy) st = nullptr;
+    constexpr int kSlots = 4096;
+    struct Slab {
+        unsigned* base = nullptr;
+        int used = 0;
+        std::map<cudaStream_t, int> slot;
+    };
+    static std::mutex mu;
+    static std::map<int, Slab> slabs;
+    std::lock_guard<std::mutex> lk(mu);
+    Slab& sl = slabs[device];
+    if (!sl.base) {
+        if (cudaMalloc(&sl.base, kSlots * 2 * sizeof(unsigned)) != cudaSuccess ||
+            cudaMemset(sl.base, 0, kSlots * 2 * sizeof(unsigned)) != cudaSuccess) {
+            cudaGetLastError();
+            sl.base = nullptr;
+            return nullptr;
+        }
+    }
+    auto it = sl.slot.find(st);
+    if (it == sl.slot.end()) {
+        if (sl.used == kSlots) return nullptr;
+        it = sl.slot.emplace(st, sl.used++).first;
+    }
+    return sl.base + 2 * it->second;
+}
+
 template <typename T>
 pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* dst, size_t batch,
                       const void* ghat, const void* mul, double scale, cudaStream_t st, long long grid_cap) {
@@ -569,9 +613,52 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
         ST_TRY(tensor_map_swz(p, d, dst, batch, &map_dst));
     }
     const long long grid = std::max<long long>(1, std::min<long long>(a.tiles, grid_cap > 0 ? std::min(grid_cap, d.max_ctas) : d.max_ctas));
+    // Launches with several tiles per CTA and several CTAs per SM hand the tiles
+    // out dynamically.  Co-resident CTAs do not share an SM evenly (measured on
+    // B200, PAFFT_PASS_TRACE: with equal tile counts the three CTAs of config 2's
+    // CONV pass retire at 0.71, 0.88 and 1.06 ms, config 5's strided CTAs between
+    // 1.1 and 1.9 ms), so the static order leaves SMs part empty for the last
+    // third of the launch; one-CTA-per-SM launches finish within 2% of each other
+    // and keep the static order (dynamic: config 2's DIF +6% time).
+    // PAFFT_DYN_MIN_TILES: tiles per CTA from which the order is dynamic (0 = never),
+    // PAFFT_DYN_MIN_OCC: resident CTAs per SM from which it is.
+    const int dyn_min = env_int("PAFFT_DYN_MIN_TILES", 4);
+    if (dyn_min > 0 && a.tiles >= (long long)dyn_min * grid && d.occ >= env_int("PAFFT_DYN_MIN_OCC", 2))
+        a.ctr = tile_counters(p->device, st);
+    if (a.ctr) ++g_dynamic_launches;
+    // profiling aid: per-CTA start/retire times and tile counts of this launch
+    // (synchronous; prints one line to stderr)
+    DevBuf trace;
+    if (env_int("PAFFT_PASS_TRACE", 0)) {
+        trace.bytes = (size_t)grid * 3 * sizeof(unsigned long long);
+        CUDA_TRY(cudaMalloc(&trace.p, trace.bytes));
+        CUDA_TRY(cudaMemsetAsync(trace.p, 0, trace.bytes, st));
+        a.trace = (unsigned long long*)trace.p;
+    }
     void* args[] = {&a, &map, &map_dst};
     CUDA_TRY(cudaLaunchKernel(d.fn, dim3((unsigned)grid), dim3(d.NT), args, d.smem, st));
     ++g_launches;
+    if (a.trace) {
+        std::vector<unsigned long long> h((size_t)grid * 3);
+        CUDA_TRY(cudaStreamSynchronize(st));
+        CUDA_TRY(cudaMemcpy(h.data(), trace.p, trace.bytes, cudaMemcpyDeviceToHost));
+        unsigned long long b0 = ~0ull, e1 = 0, tmin = ~0ull, tmax = 0;
+        std::vector<unsigned long long> ends;
+        for (long long i = 0; i < grid; ++i) {
+            b0 = std::min(b0, h[3 * i]);
+            e1 = std::max(e1, h[3 * i + 1]);
+            tmin = std::min(tmin, h[3 * i + 2]);
+            tmax = std::max(tmax, h[3 * i + 2]);
+            ends.push_back(h[3 * i + 1]);
+        }
+        std::sort(ends.begin(), ends.end());
+        auto q = [&](double f) { return (double)(ends[(size_t)(f * (ends.size() - 1))] - b0) * 1e-3; };
+        fprintf(stderr,
+                "[pass trace] kind %d R %d grid %lld tiles %lld dyn %d: span %.1f us; CTA retire times (us after first "
+                "start) min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f; tiles per CTA %llu..%llu\n",
+                d.kind, d.R, grid, a.tiles, a.ctr ? 1 : 0, (double)(e1 - b0) * 1e-3, q(0), q(0.1), q(0.5), q(0.9), q(1.0),
+                tmin, tmax);
+    }
     return PAFFT_OK;
 }
 
@@ -1051,6 +1138,7 @@ const char* pafft_build_info(void) {
 uint64_t pafft_permutation_pass_count(void) { return g_perm_passes; }
 void pafft_reset_permutation_pass_count(void) { g_perm_passes = 0; }
 uint64_t pafft_kernel_launch_count(void) { return g_launches; }
+uint64_t pafft_dynamic_launch_count(void) { return g_dynamic_launches; }
 
 pafft_status pafft_digit_reverse(uint64_t j, unsigned radix, unsigned digits, uint64_t* out) {
     uint64_t bound = 1;

@@ -125,6 +125,14 @@ template <typename T> struct PassArgs {
     // removes the 8-way bank conflicts of power-of-two slot strides
     int swz;
     int swz_b1;   // box rows per row group
+    // dynamic tile order: the CTA's first tile is blockIdx.x, later ones are
+    // gridDim.x + atomicAdd(&ctr[0], 1); ctr[1] counts retired CTAs and the last
+    // one zeroes both, so the pair is clean for the stream's next launch;
+    // nullptr = the static order blockIdx.x + i * gridDim.x
+    unsigned* ctr;
+    // profiling aid (PAFFT_PASS_TRACE): per CTA {first tile wait done, retire
+    // time, tiles done} in globaltimer ns; nullptr = off
+    unsigned long long* trace;
 };
 
 // Base-r digit reversal over the digits of P = r^s (permutation.cpp:27-37).
@@ -987,54 +995,105 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>:
     }
     __syncthreads();
     const long long t0 = blockIdx.x, ts = gridDim.x;
+    // tile sequence T_0 = t0, T_i = t0 + i ts (static) or ts + atomicAdd(ctr, 1)
+    // (dynamic: CTAs that run faster take more tiles, so the launch has no
+    // ragged tail).  Warp 0 fetches T_i when it issues that tile's staging and
+    // leaves it in nxt[i & 1] for the other warps (read after a CTA barrier).
+    int* const nxt = reinterpret_cast<int*>(bars + 2);
+    const bool dyn = a.ctr != nullptr;
+    // (lane 0 keeps one ticket in hand, taken at the previous staging, so the
+    // atomic's round trip is off the refill's critical path)
+    unsigned ahead = 0;
+    if (dyn && t == 0) ahead = atomicAdd(a.ctr, 1u);
+    auto fetch = [&](int i) -> long long {  // warp 0, all lanes
+        if (!dyn) return t0 + (long long)i * ts;
+        unsigned v = 0;
+        if (lane == 0) {
+            const unsigned long long w = (unsigned long long)ts + ahead;
+            ahead = atomicAdd(a.ctr, 1u);
+            v = w < (unsigned long long)a.tiles ? (unsigned)w : (unsigned)a.tiles;
+            nxt[i & 1] = (int)v;
+        }
+        return (long long)__shfl_sync(0xffffffffu, v, 0);
+    };
     if (warp == 0) {
         if (t0 < a.tiles) stage_tile<R, W, SW, STRIDED>(a, &tmap, t0, bufs, &bars[0], lane);
-        if (NBUF == 2 && t0 + ts < a.tiles)
-            stage_tile<R, W, SW, STRIDED>(a, &tmap, t0 + ts, bufs + BUFE, &bars[1], lane);
+        if constexpr (NBUF == 2) {
+            const long long t1 = fetch(1);
+            if (t1 < a.tiles) stage_tile<R, W, SW, STRIDED>(a, &tmap, t1, bufs + BUFE, &bars[1], lane);
+        }
     }
     __syncthreads();  // hand-copied fp32 tail elements of the first tiles
 
     // Deferred refill: after storing tile i from buffer b, the refill of b
     // with tile i+2 waits for the store to drain shared memory; warp 0 does
     // that after the next tile's first barrier instead of stalling the CTA.
-    long long pend = -1;
+    int pend = -1;  // sequence index of the tile to stage, -1 = none
     V* pbuf = nullptr;
     unsigned long long* pbar = nullptr;
     auto service = [&]() {
         if (warp == 0 && pend >= 0) {
-            if (lane == 0) bulk_wait_read0();
-            __syncwarp();
-            fence_proxy_async();
-            stage_tile<R, W, SW, STRIDED>(a, &tmap, pend, pbuf, pbar, lane);
-            // (the instruction-cache-bound 25-point kernels, config 5, lose ~1%
-            // to the extra code, so they skip it)
-            if constexpr (KIND == KIND_CONV && PAFFT_GHAT_PF && FA::FMAX < 25) {
-                if (lane == 0) prefetch_filter_blocks<R, W>(a, pend);
+            const long long nt = fetch(pend);
+            if (nt < a.tiles) {
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+                fence_proxy_async();
+                stage_tile<R, W, SW, STRIDED>(a, &tmap, nt, pbuf, pbar, lane);
+                // (the instruction-cache-bound 25-point kernels, config 5, lose ~1%
+                // to the extra code, so they skip it)
+                if constexpr (KIND == KIND_CONV && PAFFT_GHAT_PF && FA::FMAX < 25) {
+                    if (lane == 0) prefetch_filter_blocks<R, W>(a, nt);
+                }
             }
         }
         pend = -1;
     };
+    unsigned long long trace_t0 = 0;
+    if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace_t0));
     int it = 0;
-    for (long long tile = t0; tile < a.tiles; tile += ts, ++it) {
+    for (long long tile = t0; tile < a.tiles; ++it) {
         const int b = NBUF == 2 ? (it & 1) : 0;
         V* const buf = bufs + b * BUFE;
         run_tile<T, RADIX, FA, KIND, MAP, Pol, Pol::NTB == Pol::NT>(a, &tmap_dst, tile, buf, bufs + NBUF * BUFE, t,
                                                                     service, &bars[b],
                                                                     NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
-        if (tile + NBUF * ts < a.tiles) {
-            pend = tile + NBUF * ts;
+        // this buffer's next tile is T_{it + NBUF} (staged only if it exists)
+        if (dyn || t0 + (long long)(it + NBUF) * ts < a.tiles) {
+            pend = it + NBUF;
             pbuf = buf;
             pbar = &bars[b];
         }
         // no later barrier in the next tile (or the next tile is this refill)
         if constexpr (!TSTORE || NS == 1 || NBUF == 1) service();
         // single buffer: an fp32 tail element hand-copied by the refill must be
-        // visible before the next tile's first shared-memory reads
-        if constexpr (NBUF == 1 && sizeof(V) == 8) __syncthreads();
+        // visible before the next tile's first shared-memory reads (and, in
+        // dynamic order, the next tile's index)
+        if constexpr (NBUF == 1) {
+            if (sizeof(V) == 8 || dyn) __syncthreads();
+        }
+        // T_{it+1}: fetched by the prologue or by a service() that ran before
+        // this tile's last barrier (NBUF == 1: the barrier above)
+        tile = dyn ? (long long)nxt[(it + 1) & 1] : t0 + (long long)(it + 1) * ts;
     }
     service();
     if constexpr (TSTORE) {
         if (t == 0) bulk_wait0();  // stores complete before the CTA retires
+    }
+    if (a.trace && t == 0) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        a.trace[3 * blockIdx.x] = trace_t0;
+        a.trace[3 * blockIdx.x + 1] = t1;
+        a.trace[3 * blockIdx.x + 2] = (unsigned long long)it;
+    }
+    if (dyn && t == 0) {
+        // every fetch of this CTA precedes this increment: the last CTA to
+        // arrive resets the pair
+        __threadfence();
+        if (atomicAdd(a.ctr + 1, 1u) == gridDim.x - 1) {
+            a.ctr[0] = 0;
+            a.ctr[1] = 0;
+        }
     }
 }
 
