@@ -34,6 +34,51 @@ template <> struct Cplx<double> { using type = double2; };
 template <> struct Cplx<float> { using type = float2; };
 template <typename T> using cplx = typename Cplx<T>::type;
 
+// fp32 complex arithmetic on Blackwell's packed fp32 pipe: one complex value is
+// one 64-bit register pair, add.f32x2 / mul.f32x2 / fma.f32x2 (FADD2, FMUL2,
+// FFMA2) work on both halves at once and take broadcast, swap and per-half sign
+// operand modifiers, so a complex add is one instruction instead of two, a
+// real-constant multiply-add one instead of two and a complex multiply two or
+// three instead of four.  The pipe's lane throughput is that of scalar FFMA
+// (tools/probes/ffma2.cu): what is saved is issue slots, which bound the fp32
+// passes (85% of the fp32 CONV's instructions were FFMA/FADD/FMUL).
+#ifndef PAFFT_F32X2
+#define PAFFT_F32X2 1
+#endif
+#if PAFFT_F32X2
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, float2{-b.x, -b.y}); }
+// a * b = a.x (b.x, b.y) + (-s.x, s.y), s = a.y (b.y, b.x): FMUL2 with a
+// broadcast and a swapped operand, then FFMA2 whose addend takes the per-half
+// sign as an operand modifier -- two instructions, no register moves
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    const float2 s = __fmul2_rn(float2{a.y, a.y}, float2{b.y, b.x});
+    return __ffma2_rn(float2{a.x, a.x}, b, float2{-s.x, s.y});
+}
+// a * conj(b) = a.y (b.y, b.x) + (t.x, -t.y), t = a.x (b.x, b.y)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    const float2 t = __fmul2_rn(float2{a.x, a.x}, b);
+    return __ffma2_rn(float2{a.y, a.y}, float2{b.y, b.x}, float2{t.x, -t.y});
+}
+#endif
+// a + s b, a - s b, s b for a real s (both halves the same factor)
+template <typename V, typename T> __device__ __forceinline__ V caxpy(V a, T s, V b) {
+    if constexpr (PAFFT_F32X2 && sizeof(T) == 4) return __ffma2_rn(float2{s, s}, b, a);
+    else return V{a.x + s * b.x, a.y + s * b.y};
+}
+template <typename V, typename T> __device__ __forceinline__ V cscale(T s, V b) {
+    if constexpr (PAFFT_F32X2 && sizeof(T) == 4) return __fmul2_rn(float2{s, s}, b);
+    else return V{s * b.x, s * b.y};
+}
+// a - i s b = (a.x + s b.y, a.y - s b.x)  and  a + i s b
+template <typename V, typename T> __device__ __forceinline__ V caxpy_mi(V a, T s, V b) {
+    if constexpr (PAFFT_F32X2 && sizeof(T) == 4) return __ffma2_rn(float2{s, -s}, float2{b.y, b.x}, a);
+    else return V{a.x + s * b.y, a.y - s * b.x};
+}
+template <typename V, typename T> __device__ __forceinline__ V caxpy_pi(V a, T s, V b) {
+    if constexpr (PAFFT_F32X2 && sizeof(T) == 4) return __ffma2_rn(float2{-s, s}, float2{b.y, b.x}, a);
+    else return V{a.x - s * b.y, a.y + s * b.x};
+}
 template <typename V> __device__ __forceinline__ V cadd(V a, V b) { return V{a.x + b.x, a.y + b.y}; }
 template <typename V> __device__ __forceinline__ V csub(V a, V b) { return V{a.x - b.x, a.y - b.y}; }
 // a * b
@@ -60,14 +105,26 @@ template <int E, int S, typename V> __device__ __forceinline__ V rot8(V a) {
     using T = decltype(a.x);
     constexpr int e = ((E * S) % 8 + 8) % 8;
     const T h = (T)PAFFT_SQRTH;
-    if constexpr (e == 0) return a;
-    else if constexpr (e == 1) return V{(a.x + a.y) * h, (a.y - a.x) * h};    // (1 - i)/sqrt2
-    else if constexpr (e == 2) return V{a.y, -a.x};                            // -i
-    else if constexpr (e == 3) return V{(a.y - a.x) * h, -(a.x + a.y) * h};   // (-1 - i)/sqrt2
-    else if constexpr (e == 4) return V{-a.x, -a.y};
-    else if constexpr (e == 5) return V{-(a.x + a.y) * h, (a.x - a.y) * h};   // (-1 + i)/sqrt2
-    else if constexpr (e == 6) return V{-a.y, a.x};                            // +i
-    else return V{(a.x - a.y) * h, (a.x + a.y) * h};                           // (1 + i)/sqrt2
+    if constexpr (PAFFT_F32X2 && sizeof(T) == 4) {
+        // odd eighth turns as h (a +- (-i a)): two packed instructions
+        if constexpr (e == 0) return a;
+        else if constexpr (e == 1) return cscale(h, cadd(a, V{a.y, -a.x}));    // (1 - i)/sqrt2
+        else if constexpr (e == 2) return V{a.y, -a.x};                          // -i
+        else if constexpr (e == 3) return cscale(h, csub(V{a.y, -a.x}, a));    // (-1 - i)/sqrt2
+        else if constexpr (e == 4) return V{-a.x, -a.y};
+        else if constexpr (e == 5) return cscale((T)-h, cadd(a, V{a.y, -a.x}));  // (-1 + i)/sqrt2
+        else if constexpr (e == 6) return V{-a.y, a.x};                          // +i
+        else return cscale(h, csub(a, V{a.y, -a.x}));                           // (1 + i)/sqrt2
+    } else {
+        if constexpr (e == 0) return a;
+        else if constexpr (e == 1) return V{(a.x + a.y) * h, (a.y - a.x) * h};    // (1 - i)/sqrt2
+        else if constexpr (e == 2) return V{a.y, -a.x};                            // -i
+        else if constexpr (e == 3) return V{(a.y - a.x) * h, -(a.x + a.y) * h};   // (-1 - i)/sqrt2
+        else if constexpr (e == 4) return V{-a.x, -a.y};
+        else if constexpr (e == 5) return V{-(a.x + a.y) * h, (a.x - a.y) * h};   // (-1 + i)/sqrt2
+        else if constexpr (e == 6) return V{-a.y, a.x};                            // +i
+        else return V{(a.x - a.y) * h, (a.x + a.y) * h};                           // (1 + i)/sqrt2
+    }
 }
 
 // a * exp(-2 pi i S e / P) with compile-time P, e.
@@ -111,10 +168,17 @@ template <int S> struct Dft<3, S> {
         const V a = z[OFF];
         const V t1 = cadd(z[OFF + ST], z[OFF + 2 * ST]);
         const V t2 = csub(z[OFF + ST], z[OFF + 2 * ST]);
-        const V m{a.x - (T)0.5 * t1.x, a.y - (T)0.5 * t1.y};
-        z[OFF] = cadd(a, t1);
-        z[OFF + ST] = V{m.x + s * t2.y, m.y - s * t2.x};
-        z[OFF + 2 * ST] = V{m.x - s * t2.y, m.y + s * t2.x};
+        if constexpr (PAFFT_F32X2 && sizeof(T) == 4) {
+            const V m = caxpy(a, (T)-0.5, t1);
+            z[OFF] = cadd(a, t1);
+            z[OFF + ST] = caxpy_mi(m, s, t2);
+            z[OFF + 2 * ST] = caxpy_pi(m, s, t2);
+        } else {
+            const V m{a.x - (T)0.5 * t1.x, a.y - (T)0.5 * t1.y};
+            z[OFF] = cadd(a, t1);
+            z[OFF + ST] = V{m.x + s * t2.y, m.y - s * t2.x};
+            z[OFF + 2 * ST] = V{m.x - s * t2.y, m.y + s * t2.x};
+        }
     }
 };
 
@@ -140,16 +204,28 @@ template <int S> struct Dft<5, S> {
         const V a = z[OFF];
         const V t1 = cadd(z[OFF + ST], z[OFF + 4 * ST]), t2 = cadd(z[OFF + 2 * ST], z[OFF + 3 * ST]);
         const V t3 = csub(z[OFF + ST], z[OFF + 4 * ST]), t4 = csub(z[OFF + 2 * ST], z[OFF + 3 * ST]);
-        const V m1{a.x + c1 * t1.x + c2 * t2.x, a.y + c1 * t1.y + c2 * t2.y};
-        const V m2{a.x + c2 * t1.x + c1 * t2.x, a.y + c2 * t1.y + c1 * t2.y};
-        const V n1{s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y};
-        const V n2{s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y};
-        z[OFF] = V{a.x + t1.x + t2.x, a.y + t1.y + t2.y};
         // Z1 = m1 - i n1, Z4 = m1 + i n1, Z2 = m2 - i n2, Z3 = m2 + i n2
-        z[OFF + ST] = V{m1.x + n1.y, m1.y - n1.x};
-        z[OFF + 4 * ST] = V{m1.x - n1.y, m1.y + n1.x};
-        z[OFF + 2 * ST] = V{m2.x + n2.y, m2.y - n2.x};
-        z[OFF + 3 * ST] = V{m2.x - n2.y, m2.y + n2.x};
+        if constexpr (PAFFT_F32X2 && sizeof(T) == 4) {
+            const V m1 = caxpy(caxpy(a, c1, t1), c2, t2);
+            const V m2 = caxpy(caxpy(a, c2, t1), c1, t2);
+            const V n1 = caxpy(cscale(s1, t3), s2, t4);
+            const V n2 = caxpy(cscale(s2, t3), (T)-s1, t4);
+            z[OFF] = cadd(cadd(a, t1), t2);
+            z[OFF + ST] = caxpy_mi(m1, (T)1, n1);
+            z[OFF + 4 * ST] = caxpy_pi(m1, (T)1, n1);
+            z[OFF + 2 * ST] = caxpy_mi(m2, (T)1, n2);
+            z[OFF + 3 * ST] = caxpy_pi(m2, (T)1, n2);
+        } else {
+            const V m1{a.x + c1 * t1.x + c2 * t2.x, a.y + c1 * t1.y + c2 * t2.y};
+            const V m2{a.x + c2 * t1.x + c1 * t2.x, a.y + c2 * t1.y + c1 * t2.y};
+            const V n1{s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y};
+            const V n2{s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y};
+            z[OFF] = V{a.x + t1.x + t2.x, a.y + t1.y + t2.y};
+            z[OFF + ST] = V{m1.x + n1.y, m1.y - n1.x};
+            z[OFF + 4 * ST] = V{m1.x - n1.y, m1.y + n1.x};
+            z[OFF + 2 * ST] = V{m2.x + n2.y, m2.y - n2.x};
+            z[OFF + 3 * ST] = V{m2.x - n2.y, m2.y + n2.x};
+        }
     }
 };
 

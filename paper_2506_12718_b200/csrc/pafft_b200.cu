@@ -626,7 +626,8 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     if (dyn_min > 0 && a.tiles >= (long long)dyn_min * grid && d.occ >= env_int("PAFFT_DYN_MIN_OCC", 2))
         a.ctr = tile_counters(p->device, st);
     if (a.ctr) ++g_dynamic_launches;
-    // profiling aid: per-CTA start/retire times and tile counts of this launch
+#if PAFFT_TRACE
+    // profiling build: per-CTA start/retire times and tile counts of this launch
     // (synchronous; prints one line to stderr)
     DevBuf trace;
     if (env_int("PAFFT_PASS_TRACE", 0)) {
@@ -635,9 +636,11 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
         CUDA_TRY(cudaMemsetAsync(trace.p, 0, trace.bytes, st));
         a.trace = (unsigned long long*)trace.p;
     }
+#endif
     void* args[] = {&a, &map, &map_dst};
     CUDA_TRY(cudaLaunchKernel(d.fn, dim3((unsigned)grid), dim3(d.NT), args, d.smem, st));
     ++g_launches;
+#if PAFFT_TRACE
     if (a.trace) {
         std::vector<unsigned long long> h((size_t)grid * 3);
         CUDA_TRY(cudaStreamSynchronize(st));
@@ -659,6 +662,7 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
                 d.kind, d.R, grid, a.tiles, a.ctr ? 1 : 0, (double)(e1 - b0) * 1e-3, q(0), q(0.1), q(0.5), q(0.9), q(1.0),
                 tmin, tmax);
     }
+#endif
     return PAFFT_OK;
 }
 

@@ -67,6 +67,11 @@
 #ifndef PAFFT_GHAT_PF
 #define PAFFT_GHAT_PF 1
 #endif
+// profiling build: per-CTA retire times of every pass launch (PAFFT_PASS_TRACE=1
+// at run time); off in the product build, where it would cost registers
+#ifndef PAFFT_TRACE
+#define PAFFT_TRACE 0
+#endif
 #ifndef PAFFT_SB_MAX_MINB
 #define PAFFT_SB_MAX_MINB 8
 #endif
@@ -130,9 +135,11 @@ template <typename T> struct PassArgs {
     // one zeroes both, so the pair is clean for the stream's next launch;
     // nullptr = the static order blockIdx.x + i * gridDim.x
     unsigned* ctr;
-    // profiling aid (PAFFT_PASS_TRACE): per CTA {first tile wait done, retire
-    // time, tiles done} in globaltimer ns; nullptr = off
+#if PAFFT_TRACE
+    // profiling build (-DPAFFT_TRACE=1, tools/trace_build.sh): per CTA {start,
+    // retire time, tiles done} in globaltimer ns; nullptr = off
     unsigned long long* trace;
+#endif
 };
 
 // Base-r digit reversal over the digits of P = r^s (permutation.cpp:27-37).
@@ -1048,8 +1055,13 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>:
         }
         pend = -1;
     };
-    unsigned long long trace_t0 = 0;
-    if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace_t0));
+#if PAFFT_TRACE
+    if (a.trace && t == 0) {  // straight to memory: no register lives across the tile loop
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        a.trace[3 * blockIdx.x] = now;
+    }
+#endif
     int it = 0;
     for (long long tile = t0; tile < a.tiles; ++it) {
         const int b = NBUF == 2 ? (it & 1) : 0;
@@ -1079,13 +1091,14 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>:
     if constexpr (TSTORE) {
         if (t == 0) bulk_wait0();  // stores complete before the CTA retires
     }
+#if PAFFT_TRACE
     if (a.trace && t == 0) {
         unsigned long long t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        a.trace[3 * blockIdx.x] = trace_t0;
         a.trace[3 * blockIdx.x + 1] = t1;
         a.trace[3 * blockIdx.x + 2] = (unsigned long long)it;
     }
+#endif
     if (dyn && t == 0) {
         // every fetch of this CTA precedes this increment: the last CTA to
         // arrive resets the pair

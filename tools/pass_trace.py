@@ -1,6 +1,6 @@
 """Per-CTA retire times of each pass launch (PAFFT_PASS_TRACE=1), static and
 dynamic tile order: how ragged is the tail of a persistent launch?
-python tools/pass_trace.py --config 5 --precision f64"""
+PAFFT_LIB=ab/libtrace.so python tools/pass_trace.py --config 5 --precision f64  (tools/trace_build.sh builds it)"""
 import argparse
 import os
 import sys
