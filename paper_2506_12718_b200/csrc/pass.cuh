@@ -480,6 +480,20 @@ template <typename FA, int I> struct SmallQ {
     static constexpr bool on = PAFFT_SMALLQ && I < FA::NS - 1 && FA::Q(I) > 1 && FA::Q(I) <= 3 &&
                                FA::f(I) <= 9 && FA::G(I) == FA::GMIN;
 };
+// The lo-major thread map alone (no constant twiddles) for fp32 steps of odd
+// P_I with a short inner run Q_I: in the natural map a half-warp reads
+// Q_I-long runs that start P_I elements apart, and for 5 <= Q_I < 16 those runs
+// land on overlapping 8-byte bank pairs (config 5 fp32's 25-point step with
+// Q = 5: 37% of the CONV pass's shared wavefronts were conflicts); lo-major,
+// consecutive lanes are P_I elements apart, and an odd P_I visits 16 distinct
+// bank pairs.  (fp64 tiles of these shapes measured conflict-free as they are.)
+#ifndef PAFFT_LOMAJOR
+#define PAFFT_LOMAJOR 1
+#endif
+template <typename FA, int I, int ESZ> struct LoMajor {
+    static constexpr bool on = PAFFT_LOMAJOR && ESZ == 8 && !SmallQ<FA, I>::on && I < FA::NS - 1 && FA::Q(I) > 1 &&
+                               FA::Q(I) < 16 && (FA::P(I) & 1) && FA::G(I) == FA::GMIN;
+};
 template <int F, int P, int L, int S, typename V> __device__ __forceinline__ void twiddle_lo(V (&z)[F]) {
     static_for<1, F>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
@@ -739,7 +753,8 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
 #pragma unroll
             for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
                 constexpr bool SQ = SmallQ<FA, I>::on;
-                int g = SQ ? (gt % (FA::G(I) / QI)) * QI + gt / (FA::G(I) / QI) : gt + j * GMIN;
+                constexpr bool LM = SQ || (!STRIDED && LoMajor<FA, I, (int)sizeof(V)>::on);
+                int g = LM ? (gt % (FA::G(I) / QI)) * QI + gt / (FA::G(I) / QI) : gt + j * GMIN;
                 if constexpr (WSCAT && I == NS - 1) g = kScatter<FA, RADIX, GPWS>.sigma[gt];
                 const int hi = g / QI, lo = g - (g / QI) * QI;
                 const int sb = hi * PI + lo;
@@ -858,7 +873,8 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
 #pragma unroll
                 for (int j = 0; j < (act ? FA::G(I) / GMIN : 0); ++j) {
                     constexpr bool SQ = SmallQ<FA, I>::on;
-                    const int g = SQ ? (gt % (FA::G(I) / QI)) * QI + gt / (FA::G(I) / QI) : gt + j * GMIN;
+                    constexpr bool LM = SQ || (!STRIDED && LoMajor<FA, I, (int)sizeof(V)>::on);
+                    const int g = LM ? (gt % (FA::G(I) / QI)) * QI + gt / (FA::G(I) / QI) : gt + j * GMIN;
                     const int hi = g / QI, lo = g - (g / QI) * QI;
                     const int sb = hi * PI + lo;
                     V z[FI];
