@@ -631,7 +631,7 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     // (synchronous; prints one line to stderr)
     DevBuf trace;
     if (env_int("PAFFT_PASS_TRACE", 0)) {
-        trace.bytes = (size_t)grid * 3 * sizeof(unsigned long long);
+        trace.bytes = (size_t)grid * 4 * sizeof(unsigned long long);
         CUDA_TRY(cudaMalloc(&trace.p, trace.bytes));
         CUDA_TRY(cudaMemsetAsync(trace.p, 0, trace.bytes, st));
         a.trace = (unsigned long long*)trace.p;
@@ -642,25 +642,29 @@ pafft_status launch_t(pafft_plan_t p, const PassDesc& d, const void* src, void* 
     ++g_launches;
 #if PAFFT_TRACE
     if (a.trace) {
-        std::vector<unsigned long long> h((size_t)grid * 3);
+        std::vector<unsigned long long> h((size_t)grid * 4);
         CUDA_TRY(cudaStreamSynchronize(st));
         CUDA_TRY(cudaMemcpy(h.data(), trace.p, trace.bytes, cudaMemcpyDeviceToHost));
         unsigned long long b0 = ~0ull, e1 = 0, tmin = ~0ull, tmax = 0;
         std::vector<unsigned long long> ends;
+        double wait_frac = 0;
         for (long long i = 0; i < grid; ++i) {
-            b0 = std::min(b0, h[3 * i]);
-            e1 = std::max(e1, h[3 * i + 1]);
-            tmin = std::min(tmin, h[3 * i + 2]);
-            tmax = std::max(tmax, h[3 * i + 2]);
-            ends.push_back(h[3 * i + 1]);
+            b0 = std::min(b0, h[4 * i]);
+            e1 = std::max(e1, h[4 * i + 1]);
+            tmin = std::min(tmin, h[4 * i + 2]);
+            tmax = std::max(tmax, h[4 * i + 2]);
+            ends.push_back(h[4 * i + 1]);
+            wait_frac += (double)h[4 * i + 3] / (double)std::max<unsigned long long>(1, h[4 * i + 1] - h[4 * i]);
         }
+        wait_frac /= (double)grid;
         std::sort(ends.begin(), ends.end());
         auto q = [&](double f) { return (double)(ends[(size_t)(f * (ends.size() - 1))] - b0) * 1e-3; };
         fprintf(stderr,
                 "[pass trace] kind %d R %d grid %lld tiles %lld dyn %d: span %.1f us; CTA retire times (us after first "
-                "start) min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f; tiles per CTA %llu..%llu\n",
+                "start) min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f; tiles per CTA %llu..%llu; waiting for tile "
+                "arrival %.1f%% of CTA time\n",
                 d.kind, d.R, grid, a.tiles, a.ctr ? 1 : 0, (double)(e1 - b0) * 1e-3, q(0), q(0.1), q(0.5), q(0.9), q(1.0),
-                tmin, tmax);
+                tmin, tmax, 100.0 * wait_frac);
     }
 #endif
     return PAFFT_OK;

@@ -137,7 +137,7 @@ template <typename T> struct PassArgs {
     unsigned* ctr;
 #if PAFFT_TRACE
     // profiling build (-DPAFFT_TRACE=1, tools/trace_build.sh): per CTA {start,
-    // retire time, tiles done} in globaltimer ns; nullptr = off
+    // retire time, tiles done, time waiting for tile arrival} in globaltimer ns; nullptr = off
     unsigned long long* trace;
 #endif
 };
@@ -738,7 +738,20 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
             }
         }
     }
+#if PAFFT_TRACE
+    // profiling build: time thread 0 spends waiting for the tile to arrive
+    // (accumulated in trace[4 bid + 3])
+    unsigned long long tw0 = 0;
+    if (a.trace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw0));
+#endif
     if (tile_bar) mbar_wait(tile_bar, tile_phase);
+#if PAFFT_TRACE
+    if (a.trace && t == 0) {
+        unsigned long long tw1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw1));
+        a.trace[4 * blockIdx.x + 3] += tw1 - tw0;
+    }
+#endif
 
     // DIF results of the last step, held until every thread has read its
     // last-step inputs (the output rows pos(k) belong to other groups)
@@ -1075,7 +1088,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>:
     if (a.trace && t == 0) {  // straight to memory: no register lives across the tile loop
         unsigned long long now;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-        a.trace[3 * blockIdx.x] = now;
+        a.trace[4 * blockIdx.x] = now;
     }
 #endif
     int it = 0;
@@ -1111,8 +1124,8 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>:
     if (a.trace && t == 0) {
         unsigned long long t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        a.trace[3 * blockIdx.x + 1] = t1;
-        a.trace[3 * blockIdx.x + 2] = (unsigned long long)it;
+        a.trace[4 * blockIdx.x + 1] = t1;
+        a.trace[4 * blockIdx.x + 2] = (unsigned long long)it;
     }
 #endif
     if (dyn && t == 0) {

@@ -23,7 +23,7 @@ N, B = cfg.total, (cfg.batch if a.config != 1 else 1)
 filt = pf.prepare_filter_from_impulse(torch.randn(N, dtype=cdt, device="cuda"), plan)
 x = torch.rand(B, N, dtype=cdt, device="cuda")
 y = torch.empty_like(x)
-for dyn in (0, 2):
+for dyn in (0, 4):
     os.environ["PAFFT_DYN_MIN_TILES"] = str(dyn)
     os.environ["PAFFT_PASS_TRACE"] = "0"
     for _ in range(3):
