@@ -1099,7 +1099,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>:
                                                                     service, &bars[b],
                                                                     NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
         // this buffer's next tile is T_{it + NBUF} (staged only if it exists)
-        if (dyn || t0 + (long long)(it + NBUF) * ts < a.tiles) {
+        if (dyn || tile + NBUF * ts < a.tiles) {
             pend = it + NBUF;
             pbuf = buf;
             pbar = &bars[b];
@@ -1114,7 +1114,7 @@ __global__ void __launch_bounds__(TilePolicy<T, Fac<F0, F1, F2, F3>, MAP, WOVR>:
         }
         // T_{it+1}: fetched by the prologue or by a service() that ran before
         // this tile's last barrier (NBUF == 1: the barrier above)
-        tile = dyn ? (long long)nxt[(it + 1) & 1] : t0 + (long long)(it + 1) * ts;
+        tile = dyn ? (long long)nxt[(it + 1) & 1] : tile + ts;
     }
     service();
     if constexpr (TSTORE) {
