@@ -26,11 +26,15 @@ def _port():
 
 def test_two_rank_bench_line_strong_partition():
     env = dict(os.environ, PAFFT_BENCH_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--config", "5", "--batch", "64", "--steps", "2", "--warmup", "3",
-           "--no-cpu", "--no-e2e", "--no-sub"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    for attempt in range(3):
+        # the free port found here can be taken again before torchrun binds it: try another one
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
+               "--gpus", "2", "--config", "5", "--batch", "64", "--steps", "2", "--warmup", "3",
+               "--no-cpu", "--no-e2e", "--no-sub"]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
+            break
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout  # rank 0 only

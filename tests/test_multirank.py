@@ -55,10 +55,16 @@ def _worker(rank, world, port, out):
 
 def test_sharding_and_filter_broadcast_gloo():
     world = 2
-    port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    for attempt in range(3):
+        # the free port found here can be taken again before gloo binds it: try another one
+        try:
+            mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+            break
+        except Exception as e:
+            if attempt == 2 or not ("EADDRINUSE" in str(e) or "address already in use" in str(e).lower()):
+                raise
     from paper_2506_12718_b200 import workload
     cfg = workload.Config(0, "t", 3, [243], 5, "uniform", "cnormal")
     r0, r1 = out[0], out[1]
