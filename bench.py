@@ -44,7 +44,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 KIND_NAMES = {0: "dif", 1: "dit_fwd", 2: "dit_conj", 3: "conv_mid"}
-SUB_CONFIGS = [(1, "f64"), (3, "f64"), (4, "f64"), (5, "f64"), (5, "f32")]
+SUB_CONFIGS = [(1, "f64"), (3, "f64"), (4, "f64"), (5, "f64"), (5, "f32"), (2, "f32")]
 # measured FP peaks (tools/probes/peaks.cu, profiles/r01_peaks_probe.log): DFMA / FFMA TFLOP/s
 FP_PEAK = {"f64": 34.08, "f32": 72.06}
 

@@ -305,6 +305,23 @@ void build_groups(pafft_plan_t p) {
         const int max_mid = std::min(maxs, env_int("PAFFT_MAX_MID_STAGES", maxs));
         int max_str = max_stages_compiled(p->prec, (int)radix, KIND_DIF, MAP_STRIDED);
         if (radix == 2) max_str = std::min(max_str, 11);
+        // fp32 strided rows of an odd number of elements (odd radix, all lower
+        // extents odd) alternate between 16-byte aligned and misaligned starts, so
+        // no tensor map describes them and each row is staged by its own bulk
+        // copy.  That needs long rows: the 729- and 625-row groups (81 / 125
+        // threads per column) are held to 8 columns by the 1024-thread limit, 80-byte
+        // copies that run at ~0.5 TB/s, while 16-column groups reach ~3 TB/s and
+        // single-codelet ones (64 columns) the HBM roof.  Such axes therefore stop
+        // at 81 / 125 rows per strided pass (measured: 243 rows in one pass is 21%
+        // slower than 9 + 27) and take one more round trip each way instead:
+        // config 2 in fp32 9.6k -> 38.0k conv/s, 5^9 2.6x, 729 x 729 3.9x
+        // (profiles/r02_f32_odd_schedule.log).
+        {
+            unsigned long long sq = 1;
+            for (int i = 0; i < q; ++i) sq *= (unsigned long long)p->dims[i];
+            if (p->esize == 8 && (radix & 1) && (sq & 1) && env_int("PAFFT_F32_ODD_SINGLE", 1))
+                max_str = std::min(max_str, radix == 3 ? 4 : 3);
+        }
         max_str = std::min(max_str, env_int("PAFFT_MAX_STRIDED_STAGES", max_str));
         const int lim = (q == 0) ? std::max(max_mid, 1) : std::max(max_str, 1);
         const int forced_mid = env_int("PAFFT_MID_STAGES", 0);
