@@ -248,7 +248,20 @@ template <typename T, typename FAC, int MAP, int WOVR = 0> struct TilePolicy {
     static constexpr int MINB_REG = 65536 / (((NT + 31) / 32 * 32) * REG_FLOOR);
     static constexpr int MAXB = NBUF == 1 ? (MINB_REG < PAFFT_SB_MAX_MINB ? MINB_REG : PAFFT_SB_MAX_MINB)
                                           : PAFFT_MAX_MINB;
-    static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > MAXB ? MAXB : MINB_SMEM);
+    static constexpr int MINB0 = MINB_SMEM < 1 ? 1 : (MINB_SMEM > MAXB ? MAXB : MINB_SMEM);
+    // fp32 contiguous tiles of many threads: do not let the occupancy the shared
+    // memory allows push the register allocation below ~2/3 of the fp64 floor
+    // (config 2 fp32's 486-thread CONV tiles at three CTAs per SM got 40
+    // registers and spilled 84 bytes per thread into an L1 that is the pass's
+    // limiter)
+#ifndef PAFFT_F32_REGCAP
+#define PAFFT_F32_REGCAP 1
+#endif
+    static constexpr int MINB_F32 = 65536 / (((NT + 31) / 32 * 32) * (REG_FLOOR * 2 / 3));
+    static constexpr int MINB = (PAFFT_F32_REGCAP && ESZ == 8 && MAP == MAP_CONTIG && NBUF == 2 && MINB_F32 >= 1 &&
+                                 MINB_F32 < MINB0)
+                                    ? MINB_F32
+                                    : MINB0;
     static constexpr int NTB = NT;  // threads per block
 };
 
