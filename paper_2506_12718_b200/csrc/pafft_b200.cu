@@ -143,6 +143,7 @@ struct PassDesc {
     size_t smem = 0;
     long long max_ctas = 1;
     int occ = 1;  // resident CTAs per SM
+    int dense = 0;  // fp32 strided tile without spare row slots (even row lengths, tensor maps)
     int use_tmap = 0, rb = 0, sw = 0;  // STRIDED tensor-map staging
     int swz = 0, swz_b1 = 0;           // CONTIG 128B-swizzled staging (power-of-two radix)
     int ext = 0;
@@ -389,7 +390,8 @@ pafft_status bind_kernel(pafft_plan_t p, const KernelEntry& ke, PassDesc& d) {
     if (occ < 1) return fail(PAFFT_CUDA_ERROR, "pass kernel R=%d cannot be resident (smem %zu)", d.R, d.smem);
     d.max_ctas = (long long)occ * sms;
     d.occ = occ;
-    if (!d.contig) d.sw = p->esize == 8 ? d.W + 2 : d.W;
+    d.dense = ke.wide == 2;
+    if (!d.contig) d.sw = (p->esize == 8 && !d.dense) ? d.W + 2 : d.W;
     return PAFFT_OK;
 }
 
@@ -409,6 +411,17 @@ pafft_status make_pass(pafft_plan_t p, const Group& g, int kind, PassDesc& d) {
     d.C = d.L * sq;
     d.contig = d.C == 1;
     const KernelEntry* ke = find_kernel(p->prec, (int)radix, d.R, kind, d.contig ? MAP_CONTIG : MAP_STRIDED);
+    // 2-D tensor map staging: row groups of rb rows, at most 256 groups per box
+    int rb = 1;
+    for (int v = 1; v <= 256 && v <= d.R; ++v)
+        if (d.R % v == 0) rb = v;
+    // fp32 strided tiles of even row length whose box a tensor map can describe
+    // take the dense instance (PAFFT_F32_DENSE=0: the spare-slot one everywhere)
+    if (ke && !d.contig && p->esize == 8 && d.C % 2 == 0 && d.R / rb <= 256 && env_int("PAFFT_F32_DENSE", 1) &&
+        env_int("PAFFT_NO_TMAP", 0) == 0) {
+        const KernelEntry* de = find_kernel(p->prec, (int)radix, d.R, kind, MAP_STRIDED, 2);
+        if (de && de->F0 == ke->F0 && de->F1 == ke->F1 && de->F2 == ke->F2 && de->F3 == ke->F3) ke = de;
+    }
     if (!ke)
         return fail(PAFFT_INVALID_ARGUMENT, "no kernel for radix %u R=%d kind %d map %d", radix, d.R, kind,
                     d.contig);

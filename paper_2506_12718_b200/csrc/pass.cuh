@@ -196,7 +196,10 @@ template <typename T, typename FAC, int MAP, int WOVR = 0> struct TilePolicy {
     // fp32 strided rows may start 8 bytes off a 16-byte boundary (odd C):
     // each shared row then holds W + 2 slots and the data sits at a per-row
     // shift of 0 or 1 element (see stage_tile).
-    static constexpr bool SHIFT = MAP == MAP_STRIDED && ESZ == 8;
+    // (WOVR < 0: the dense fp32 strided instance for even row lengths -- rows are
+    // 16-byte aligned, the tile comes and goes through tensor maps like an fp64
+    // one, no spare slots, no per-row copies, no register stores)
+    static constexpr bool SHIFT = MAP == MAP_STRIDED && ESZ == 8 && WOVR >= 0;
     static constexpr int rowslots(int w) { return SHIFT ? w + 2 : w; }
     static constexpr int wcalc() {
         if (MAP == MAP_STRIDED && FAC::NS > 1) {
@@ -660,7 +663,7 @@ __device__ __forceinline__ void run_tile(const PassArgs<T>& a, const CUtensorMap
     // lane-rotated Q = 1 steps (PAFFT_ROT): fp64 strided rows narrower than 128 B
     constexpr int GQ = (STRIDED && !SHIFT && SW * (int)sizeof(V) < 128) ? 128 / (SW * (int)sizeof(V)) : 1;
     constexpr int GQB = GQ >= 8 ? 3 : GQ >= 4 ? 2 : GQ >= 2 ? 1 : 0;
-    constexpr bool ROT = PAFFT_ROT && GQ > 1 && (FL & (FL - 1)) == 0 && FL >= GQ && (32 % W == 0);
+    constexpr bool ROT = PAFFT_ROT && sizeof(V) == 16 && GQ > 1 && (FL & (FL - 1)) == 0 && FL >= GQ && (32 % W == 0);
     (void)BUFE;
     (void)buf_end;
     const int warp = t >> 5, lane = t & 31;

@@ -15,7 +15,8 @@ struct KernelEntry {
     int map;    // PassMap
     int W, NT, smem;  // compile-time tile policy of this instance
     const void* fn;
-    int wide = 0;     // 1: wide strided variant (more columns per tile) for launches with many tiles
+    int wide = 0;     // 1: wide strided variant (more columns per tile) for launches with many tiles;
+                      // 2: dense fp32 strided variant (even row lengths, tensor maps, no spare row slots)
 };
 
 using Registry = std::vector<KernelEntry>;
