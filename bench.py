@@ -585,11 +585,15 @@ def gpu_measure(g, cfg, args, steps, warmup, with_e2e, with_cpu):
         host_step()
         g.barrier()
         t = time.perf_counter()
+        step_ms = []
         for _ in range(ysteps):
-            host_step()
+            t1 = time.perf_counter()
+            host_step()  # synchronous: returns when the results are in the host buffer
+            step_ms.append(1e3 * (time.perf_counter() - t1))
         et = pdist.max_over_ranks(time.perf_counter() - t, dev)
+        # value = all timed steps (mean); the per-step times show how steady the host link was
         e2e = {"value": global_batch * ysteps / et, "unit": "conv/s", "h2d_bytes_per_step": per * S,
-               "d2h_bytes_per_step": per * S, "steps": ysteps,
+               "d2h_bytes_per_step": per * S, "steps": ysteps, "step_ms": [round(v, 3) for v in step_ms],
                "pipelined": "3 streams, 64 MiB chunks, pinned host buffers"}
         del yh
 
