@@ -140,3 +140,54 @@ def test_wide_strided_tiles_are_bitwise_the_narrow_ones(pf, torch, monkeypatch, 
     yn = pf.convolve_permfree_out(x, torch.empty_like(x), pf.prepare_filter_from_impulse(h, narrow), narrow)
     torch.cuda.synchronize()
     assert torch.equal(yw, yn)
+
+
+@pytest.mark.parametrize("radix,dims,batch", [(2, [64, 256, 8], 3), (4, [256, 64], 5), (8, [64, 512], 2),
+                                              (2, [4096, 32], 4)])
+def test_fp32_dense_strided_tiles_are_bitwise_the_spare_slot_ones(pf, torch, monkeypatch, radix, dims, batch):
+    """fp32 strided tiles of even row length take the dense instance (tensor-map
+    staging and stores, no spare row slots; pafft_b200.cu make_pass); per column
+    it does the same arithmetic as the spare-slot instance that odd row lengths
+    need, so the convolution is bitwise identical (PAFFT_F32_DENSE=0 at plan
+    creation disables it)."""
+    n = int(np.prod(dims))
+    rng = np.random.default_rng(17)
+    x = torch.from_numpy((rng.standard_normal((batch, n)) + 1j * rng.standard_normal((batch, n))).astype(np.complex64)).cuda()
+    h = torch.from_numpy((rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(np.complex64)).cuda()
+    dense = pf.Plan(radix, dims, precision=pf.F32)
+    monkeypatch.setenv("PAFFT_F32_DENSE", "0")
+    spare = pf.Plan(radix, dims, precision=pf.F32)
+    monkeypatch.delenv("PAFFT_F32_DENSE")
+    assert dense.num_passes() == spare.num_passes() >= 3
+    yd = pf.convolve_permfree_out(x, torch.empty_like(x), pf.prepare_filter_from_impulse(h, dense), dense)
+    ys = pf.convolve_permfree_out(x, torch.empty_like(x), pf.prepare_filter_from_impulse(h, spare), spare)
+    torch.cuda.synchronize()
+    assert torch.equal(yd, ys)
+
+
+def test_fp32_odd_row_lengths_take_short_strided_groups(pf, torch, orc, monkeypatch):
+    """fp32 axes whose strided rows have an odd number of elements stop at 81
+    (radix 3) / 125 (radix 5) rows per strided pass (build_groups): 3^12 runs
+    DIF 9, DIF 27, CONV 3^7, DIT 27, DIT 9 instead of DIF 243, CONV, DIT 243;
+    both schedules meet the fp32 bar against the fp64 pipeline on the rounded
+    inputs."""
+    dims = [3 ** 12]
+    n = dims[0]
+    x32 = rand_c(n, 3).astype(np.complex64)
+    h32 = rand_c(n, 4).astype(np.complex64)
+    op = orc.plan(3, dims)
+    want = op.convolve_permfree(x32.astype(np.complex128),
+                                op.prepare_filter(op.filter_from_impulse(h32.astype(np.complex128))))
+    short = pf.Plan(3, dims, precision=pf.F32)
+    monkeypatch.setenv("PAFFT_F32_ODD_SINGLE", "0")
+    long_ = pf.Plan(3, dims, precision=pf.F32)
+    monkeypatch.delenv("PAFFT_F32_ODD_SINGLE")
+    assert short.num_passes() == 5 and long_.num_passes() == 3, (short.describe(), long_.describe())
+    for plan in (short, long_):
+        xt = torch.from_numpy(x32).cuda()
+        f = pf.prepare_filter_from_impulse(torch.from_numpy(h32).cuda(), plan)
+        pf.convolve_permfree_(xt, f, plan)
+        torch.cuda.synchronize()
+        assert rel_l2(xt.cpu().numpy().astype(np.complex128), want) <= 1e-5, plan.describe()
+    # fp64 plans are not affected
+    assert pf.Plan(3, dims).num_passes() == 3
